@@ -1,0 +1,178 @@
+/*
+ * besselgp_b200.h -- C ABI of libbesselgp_sm100a.so, the B200 (sm_100a) build of
+ * the BesselK / Matern-covariance hot path of arXiv 2502.00356.
+ *
+ * Drop-in boundary.  The reference has no native code: its "operator layer" is
+ * the set of numba kernels in /root/reference/pkg/src/besselgp/kernels.py that
+ * take flat scalars plus caller-allocated arrays.  Each entry point below
+ * replaces one of them (file:line cited) over device arrays, and the Python
+ * package paper_2502_00356_b200 binds them with ctypes exactly where the
+ * reference's besselk.py calls kernels.* (see INTEGRATION.md).
+ *
+ * Conventions:
+ *   - every array argument is a DEVICE pointer (cudaMalloc / torch CUDA tensor);
+ *     the caller owns all memory, the library never allocates;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *     every call is asynchronous and stream-ordered, re-entrant, and keeps no
+ *     mutable global state (per-call tables travel as kernel parameters);
+ *   - return 0 (BGK_OK) or a negative BGK_ERR_* code; bgk_last_error() gives a
+ *     thread-local message.  Domain validation with the reference's exact
+ *     messages lives in the Python layer (besselk.py:28-29, 43-51, 65-69);
+ *     like the numba kernels, these entry points never raise on values --
+ *     garbage in gives NaN/inf out;
+ *   - results are pure functions of each element's inputs: bitwise
+ *     independent of batch size, tiling, launch geometry and shard count.
+ */
+#ifndef BESSELGP_B200_H
+#define BESSELGP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BGK_ABI_VERSION 1
+
+#define BGK_OK 0
+#define BGK_ERR_INVALID (-1)     /* bad argument (null pointer, bad size, bad enum) */
+#define BGK_ERR_CUDA (-2)        /* a CUDA runtime error (launch / config) */
+#define BGK_ERR_UNSUPPORTED (-3) /* configuration outside what the kernels support */
+
+/* QuadratureConfig (besselk.py:32-41): fixed window [t_lower, t_upper], bins
+ * trapezoid intervals, series below small_x_threshold, Temme cap / epsilon. */
+typedef struct bgk_config {
+  double t_lower;
+  double t_upper;
+  int64_t bins;
+  double small_x_threshold;
+  int64_t series_cap;
+  double eps_machine;
+} bgk_config;
+
+/* Routing for bgk_besselk_batch. */
+#define BGK_ROUTE_HYBRID 0   /* refined_log_bessel (kernels.py:296-302): x < thr -> series */
+#define BGK_ROUTE_SERIES 1   /* temme_series_log (kernels.py:273-293) for every element   */
+#define BGK_ROUTE_INTEGRAL 2 /* fixed_window_log_pair (kernels.py:212-216), no guard      */
+
+/* path[] codes (PathTaken, besselk.py:23-25) */
+#define BGK_PATH_SERIES 0
+#define BGK_PATH_INTEGRAL 1
+
+/* Matern output layouts */
+#define BGK_LAYOUT_ROW_MAJOR 0 /* element (i,j) at out[i*ld + j] (numpy C order) */
+#define BGK_LAYOUT_COL_MAJOR 1 /* element (i,j) at out[i + j*ld] (SPEC.md:283 tiles) */
+
+/* ln K_nu(x) over n elements.
+ * Replaces kernels.refined_log_bessel (kernels.py:297) / temme_series_log
+ * (kernels.py:274) / fixed_window_log_pair (kernels.py:213) as called by
+ * besselk.bessel_k (besselk.py:158-165), bessel_k_series (:104-110),
+ * fixed_window_log_bessel_k (:134-146).
+ *   log_k  required, ln K
+ *   k      optional (NULL), exp(ln K) with overflow -> +inf (besselk.py:80-84)
+ *   path   optional (NULL), BGK_PATH_* per element                       */
+int bgk_besselk_batch(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
+                      int route, double *log_k, double *k, uint8_t *path, void *stream);
+
+/* Temme starting sums (s0, s1, terms) with K_mu = s0, K_{mu+1} = (2/x) s1.
+ * Replaces kernels.temme_sums (kernels.py:230-270) as called by
+ * besselk.temme_pair (besselk.py:94-101).  terms may be NULL. */
+int bgk_temme_sums_batch(const double *x, const double *mu, int64_t n, const bgk_config *cfg,
+                         double *s0, double *s1, int64_t *terms, void *stream);
+
+/* g(t) = log cosh(nu t) - x cosh t (order 0), g' (order 1), g'' (order 2).
+ * Replaces kernels.log_integrand / _d1 / _d2 (kernels.py:52-72). */
+int bgk_log_integrand_batch(const double *t, const double *x, const double *nu, int64_t n,
+                            int order, double *out, void *stream);
+
+/* ---- Matern covariance ------------------------------------------------------------ */
+
+#define BGK_MATERN_MAX_NODES 1024
+#define BGK_MATERN_MAX_BUCKETS 1024
+
+/* Per-call plan: the restated caller's per-nu work (kernels.py:343-345,
+ * SPEC.md:306-332) hoisted out of the entry loop -- node tables
+ * c_m = cosh(t_m), a_m = log_cosh(nu t_m), the Matern log-prefactor, the
+ * nu-only Temme constants and the u-bucket -> (anchor node, node window)
+ * lookup table the kernel uses instead of a 41-node argmax scan.
+ * Caller-allocated POD (sizeof == bgk_matern_plan_size()); fill it with one of
+ * the bgk_matern_plan_init* calls; it is passed to kernels by value. */
+typedef struct bgk_matern_plan {
+  int32_t abi;      /* BGK_ABI_VERSION */
+  int32_t nnodes;   /* bins + 1 */
+  int32_t nbuckets; /* entries of lut[] */
+  int32_t key_base; /* u-bucket key of lut[0] (top 16 bits of the double) */
+  int32_t fast;     /* 1: lut path; 0: general argmax-scan path */
+  int32_t m_steps;  /* Temme: floor(nu + 0.5) */
+  double sigma_sq, beta, nu, log_prefactor, h, small_x_threshold, eps_machine;
+  int64_t series_cap;
+  double mu, gam1, gam2, fact, gamma_1p_mu, gamma_1m_mu; /* Temme, nu-only */
+  double c[BGK_MATERN_MAX_NODES];  /* cosh(t_m)                          */
+  double a[BGK_MATERN_MAX_NODES];  /* log_cosh(nu t_m)                   */
+  double aw[BGK_MATERN_MAX_NODES]; /* a_m + log(trapezoid weight w_m)    */
+  uint32_t lut[BGK_MATERN_MAX_BUCKETS]; /* anchor | lo << 10 | hi << 20 */
+} bgk_matern_plan;
+
+size_t bgk_matern_plan_size(void);
+
+/* Plan from Matern parameters + QuadratureConfig (the SPEC covariance API):
+ * tables built like the restated caller, log_prefactor =
+ * log(sigma_sq) - (nu - 1) ln2 - lgamma(nu). */
+int bgk_matern_plan_init(bgk_matern_plan *plan, double sigma_sq, double beta, double nu,
+                         const bgk_config *cfg);
+
+/* Plan from explicit tables, i.e. the exact argument list of
+ * kernels.matern_tile (kernels.py:339-340): sigma_sq, beta, nu,
+ * log_prefactor, c_nodes, a_nodes (nnodes each), h, threshold, eps, cap. */
+int bgk_matern_plan_init_tables(bgk_matern_plan *plan, double sigma_sq, double beta, double nu,
+                                double log_prefactor, const double *c_nodes,
+                                const double *a_nodes, int64_t nnodes, double h,
+                                double small_x_threshold, double eps_machine,
+                                int64_t series_cap);
+
+/* One tile: out(i,j) = Matern(|(rx_i,ry_i) - (cx_j,cy_j)|) for i < m, j < n.
+ * Replaces kernels.matern_tile (kernels.py:339-381); layout BGK_LAYOUT_*. */
+int bgk_matern_tile(const bgk_matern_plan *plan, const double *rx, const double *ry, int64_t m,
+                    const double *cx, const double *cy, int64_t n, double *out, int64_t ld,
+                    int layout, void *stream);
+
+/* Rows [row_begin, row_end) of the full N x N covariance matrix of the
+ * locations (lx, ly), i.e. one row-block shard of SPEC generate_covariance
+ * (SPEC.md:324-332).  Row row_begin is stored first: element (i, j) of the
+ * full matrix lands at out[(i-row_begin)*ld + j] (ROW_MAJOR) or
+ * out[(i-row_begin) + j*ld] (COL_MAJOR, i.e. the column block).  Inside the
+ * diagonal block [row_begin,row_end)^2 each entry pair (i,j)/(j,i) is
+ * computed once and stored twice; entries are symmetric bitwise anyway. */
+int bgk_matern_covariance(const bgk_matern_plan *plan, const double *lx, const double *ly,
+                          int64_t N, int64_t row_begin, int64_t row_end, double *out, int64_t ld,
+                          int layout, void *stream);
+
+/* Packed lower-triangle tiles (the M200 layout): tile (p, q), q <= p, of size
+ * ts x ts has linear index l = p(p+1)/2 + q and is stored column-major at
+ * out + (l - tile_begin) * ts * ts; diagonal tiles are stored complete; entries
+ * of edge tiles beyond N are left untouched.  Produces l in
+ * [tile_begin, tile_end) -- the area-balanced shard of one GPU. */
+int bgk_matern_lower_tiles(const bgk_matern_plan *plan, const double *lx, const double *ly,
+                           int64_t N, int64_t tile_size, int64_t tile_begin, int64_t tile_end,
+                           double *out, void *stream);
+
+/* ---- misc ------------------------------------------------------------------------- */
+const char *bgk_last_error(void);
+int bgk_abi_version(void);
+/* FP64-pipe peak probe: `blocks` x 256 threads, each running 8 independent DFMA
+ * chains of 16*iters steps; *dfma_per_launch receives the DFMA count (one
+ * FP64-pipe op each).  Time it with events on `stream` to get the measured FP64
+ * roofline denominator.  `scratch` must hold blocks*256 doubles. */
+int bgk_fp64_probe(double *scratch, int64_t blocks, int iters, void *stream,
+                   double *dfma_per_launch);
+
+/* Number of kernel launches issued by this library since load (for bench.py's
+ * gpu_launches accounting). */
+int64_t bgk_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BESSELGP_B200_H */

@@ -1,0 +1,327 @@
+"""Modified Bessel function of the second kind -- B200 build of besselk.py.
+
+Same public names, dataclasses, validation, messages and routing as the
+reference module (/root/reference/pkg/src/besselgp/besselk.py:1-165); the
+numeric work that the reference hands to numba (kernels.py) runs in the sm_100a
+kernels of libbesselgp_sm100a.so instead.  Small arguments (x below the
+threshold, default 0.1) use the Temme series with a log-space forward
+recurrence; everything else uses the fixed-window trapezoid log-sum-exp
+quadrature over [t_lower, t_upper] with ``bins`` intervals.
+
+Added for the GPU: ``bessel_k_batch`` (arrays / CUDA tensors in, arrays /
+CUDA tensors out), the natural unit of work for a device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import NamedTuple
+
+import numpy as np
+
+from . import _lib
+
+EPS_MACHINE = 2.0 ** -52  # kernels.py:15
+
+VALIDATED_X_MAX = 140.0  # besselk.py:19
+VALIDATED_NU_MAX = 20.0  # besselk.py:20
+
+
+class PathTaken(enum.Enum):  # besselk.py:23-25
+    SERIES = "series"
+    INTEGRAL = "integral"
+
+
+class DomainError(ValueError):  # besselk.py:28-29
+    """Input outside an operation's domain."""
+
+
+@dataclass(frozen=True)
+class QuadratureConfig:  # besselk.py:32-51
+    """Operating point of the fixed-window quadrature and series."""
+
+    t_lower: float = 0.0
+    t_upper: float = 9.0
+    bins: int = 40
+    small_x_threshold: float = 0.1
+    series_cap: int = 15000
+    eps_machine: float = EPS_MACHINE
+
+    def __post_init__(self):
+        if not self.t_lower < self.t_upper:
+            raise DomainError("t_lower must be below t_upper")
+        if self.bins < 2:
+            raise DomainError("bins must be at least 2")
+        if self.small_x_threshold <= 0:
+            raise DomainError("small_x_threshold must be positive")
+        if self.series_cap < 1:
+            raise DomainError("series_cap must be at least 1")
+
+    def to_c(self, bins: int | None = None) -> _lib.BgkConfig:
+        return _lib.BgkConfig(float(self.t_lower), float(self.t_upper),
+                              int(self.bins if bins is None else bins),
+                              float(self.small_x_threshold), int(self.series_cap),
+                              float(self.eps_machine))
+
+
+DEFAULT_CONFIG = QuadratureConfig()
+
+
+@dataclass(frozen=True)
+class EvalPoint:  # besselk.py:57-69
+    """One (x, nu) evaluation point; negative orders fold via K_{-nu} = K_nu
+    before construction."""
+
+    x: float
+    nu: float
+
+    def __post_init__(self):
+        if not (math.isfinite(self.x) and self.x >= 0.0):
+            raise DomainError(f"x must be finite and nonnegative, got {self.x!r}")
+        if not (math.isfinite(self.nu) and self.nu >= 0.0):
+            raise DomainError(f"nu must be finite and nonnegative, got {self.nu!r}")
+
+
+@dataclass(frozen=True)
+class BesselResult:  # besselk.py:72-77
+    log_value: float
+    value: float
+    path_taken: PathTaken
+    warning: str | None = field(default=None, compare=False)
+
+
+def _result(log_value: float, path: PathTaken, p: EvalPoint) -> BesselResult:  # besselk.py:80-91
+    try:
+        value = math.exp(log_value)
+    except OverflowError:
+        value = math.inf
+    warning = None
+    if p.x > VALIDATED_X_MAX or p.nu > VALIDATED_NU_MAX:
+        warning = (
+            f"(x={p.x:g}, nu={p.nu:g}) lies outside the validated region "
+            f"[0, {VALIDATED_X_MAX:g}] x (0, {VALIDATED_NU_MAX:g}]"
+        )
+    return BesselResult(log_value, value, path, warning)
+
+
+# ---------------------------------------------------------------------------------------
+# device plumbing
+# ---------------------------------------------------------------------------------------
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_handle():
+    return _torch().cuda.current_stream().cuda_stream
+
+
+def _to_device(a, device=None):
+    """float64 contiguous CUDA tensor view/copy of ``a`` (numpy, list, scalar or tensor)."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        t = a.to(dtype=torch.float64)
+        if not t.is_cuda:
+            t = t.to(device or "cuda", non_blocking=True)
+        return t.contiguous()
+    arr = np.ascontiguousarray(a, dtype=np.float64)
+    return torch.from_numpy(arr).to(device or "cuda")
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class BatchResult(NamedTuple):
+    log_value: object
+    value: object
+    path: object
+
+
+_ROUTES = {"hybrid": _lib.ROUTE_HYBRID, "series": _lib.ROUTE_SERIES,
+           "integral": _lib.ROUTE_INTEGRAL}
+
+
+def _launch_besselk(xd, nud, cfg: QuadratureConfig, route: int, want_value=True, want_path=True,
+                    bins: int | None = None):
+    torch = _torch()
+    L = _lib.lib()
+    n = xd.numel()
+    logk = torch.empty_like(xd)
+    k = torch.empty_like(xd) if want_value else None
+    path = torch.empty(n, dtype=torch.uint8, device=xd.device) if want_path else None
+    c = cfg.to_c(bins)
+    with torch.cuda.device(xd.device):
+        rc = L.bgk_besselk_batch(xd.data_ptr(), nud.data_ptr(), n, ctypes.byref(c), route,
+                                 logk.data_ptr(), _ptr(k), _ptr(path), _stream_handle())
+    _lib.check(rc, "bgk_besselk_batch")
+    return logk, k, path
+
+
+def bessel_k_batch(x, nu, cfg: QuadratureConfig = DEFAULT_CONFIG, route: str = "hybrid",
+                   validate: bool = True) -> BatchResult:
+    """K_nu(x) over arrays on the GPU.
+
+    ``x`` and ``nu`` broadcast to a common shape.  CUDA tensors in give CUDA
+    tensors out (no host round trip); anything else is copied to the device and
+    the results come back as numpy arrays.  ``route``: "hybrid" (bessel_k),
+    "series" (every element through the Temme path) or "integral" (the
+    fixed-window quadrature with no threshold guard, like
+    fixed_window_log_bessel_k).  With ``validate`` the EvalPoint / bessel_k
+    domain rules are checked for the whole batch first (one device sync).
+    """
+    torch = _torch()
+    if route not in _ROUTES:
+        raise DomainError(f"route must be one of {sorted(_ROUTES)}")
+    on_device = isinstance(x, torch.Tensor) and x.is_cuda
+    xd = _to_device(x)
+    nud = _to_device(nu, xd.device)
+    if xd.shape != nud.shape:
+        xd, nud = torch.broadcast_tensors(xd, nud)
+        xd, nud = xd.contiguous(), nud.contiguous()
+    shape = xd.shape
+    xd, nud = xd.reshape(-1), nud.reshape(-1)
+    if validate and xd.numel():
+        bad_x = ~torch.isfinite(xd) | (xd <= 0.0)
+        bad_nu = ~torch.isfinite(nud) | (nud < 0.0)
+        if route == "series":
+            bad_x |= xd >= cfg.small_x_threshold
+        if bool(bad_x.any()) or bool(bad_nu.any()):
+            i = int(torch.nonzero(bad_x | bad_nu)[0])
+            xv, nv = float(xd[i]), float(nud[i])
+            EvalPoint(xv, nv)  # raises the reference's message for non-finite / negative
+            if route == "series":
+                raise DomainError(
+                    f"series path needs 0 < x < {cfg.small_x_threshold:g}, got {xv!r}")
+            raise DomainError("x must be positive (r = 0 is handled by the Matern kernel)")
+    logk, k, path = _launch_besselk(xd, nud, cfg, _ROUTES[route])
+    logk, k, path = logk.reshape(shape), k.reshape(shape), path.reshape(shape)
+    if on_device:
+        return BatchResult(logk, k, path)
+    return BatchResult(logk.cpu().numpy(), k.cpu().numpy(), path.cpu().numpy())
+
+
+def _scalar_logk(x: float, nu: float, cfg: QuadratureConfig, route: int,
+                 bins: int | None = None) -> float:
+    xd = _to_device([x])
+    nud = _to_device([nu], xd.device)
+    logk, _, _ = _launch_besselk(xd, nud, cfg, route, want_value=False, want_path=False,
+                                 bins=bins)
+    return float(logk.cpu()[0])
+
+
+# ---------------------------------------------------------------------------------------
+# public API (besselk.py:94-165)
+# ---------------------------------------------------------------------------------------
+
+def temme_pair(x: float, mu: float, cfg: QuadratureConfig = DEFAULT_CONFIG) -> tuple[float, float]:
+    """Starting values (K_mu(x), K_{mu+1}(x)) for -0.5 <= mu < 0.5."""
+    if not 0.0 < x < cfg.small_x_threshold:
+        raise DomainError(f"temme_pair needs 0 < x < {cfg.small_x_threshold:g}, got {x!r}")
+    if not -0.5 <= mu < 0.5:
+        raise DomainError(f"mu must lie in [-0.5, 0.5), got {mu!r}")
+    s0, s1, _ = temme_sums_batch([x], [mu], cfg)
+    return float(s0[0]), (2.0 / x) * float(s1[0])
+
+
+def temme_sums_batch(x, mu, cfg: QuadratureConfig = DEFAULT_CONFIG):
+    """kernels.temme_sums over arrays: (s0, s1, terms), K_mu = s0, K_{mu+1} = (2/x) s1."""
+    torch = _torch()
+    L = _lib.lib()
+    on_device = isinstance(x, torch.Tensor) and x.is_cuda
+    xd = _to_device(x).reshape(-1)
+    mud = _to_device(mu, xd.device).reshape(-1)
+    s0 = torch.empty_like(xd)
+    s1 = torch.empty_like(xd)
+    terms = torch.empty(xd.numel(), dtype=torch.int64, device=xd.device)
+    c = cfg.to_c()
+    with torch.cuda.device(xd.device):
+        rc = L.bgk_temme_sums_batch(xd.data_ptr(), mud.data_ptr(), xd.numel(), ctypes.byref(c),
+                                    s0.data_ptr(), s1.data_ptr(), terms.data_ptr(),
+                                    _stream_handle())
+    _lib.check(rc, "bgk_temme_sums_batch")
+    if on_device:
+        return s0, s1, terms
+    return s0.cpu().numpy(), s1.cpu().numpy(), terms.cpu().numpy()
+
+
+def bessel_k_series(p: EvalPoint, cfg: QuadratureConfig = DEFAULT_CONFIG) -> BesselResult:
+    """Series path: Temme sums plus forward recurrence, log-domain."""
+    if not 0.0 < p.x < cfg.small_x_threshold:
+        raise DomainError(
+            f"series path needs 0 < x < {cfg.small_x_threshold:g}, got {p.x!r}")
+    log_k = _scalar_logk(p.x, p.nu, cfg, _lib.ROUTE_SERIES)
+    return _result(log_k, PathTaken.SERIES, p)
+
+
+def _log_integrand_call(t: float, p: EvalPoint, order: int) -> float:
+    torch = _torch()
+    L = _lib.lib()
+    td = _to_device([t])
+    xd = _to_device([p.x], td.device)
+    nd = _to_device([p.nu], td.device)
+    out = torch.empty_like(td)
+    with torch.cuda.device(td.device):
+        rc = L.bgk_log_integrand_batch(td.data_ptr(), xd.data_ptr(), nd.data_ptr(), 1, order,
+                                       out.data_ptr(), _stream_handle())
+    _lib.check(rc, "bgk_log_integrand_batch")
+    return float(out.cpu()[0])
+
+
+def log_integrand(t: float, p: EvalPoint) -> float:
+    """g(t) = log cosh(nu t) - x cosh(t)."""
+    if t < 0.0:
+        raise DomainError("t must be nonnegative")
+    if p.x <= 0.0:
+        raise DomainError("x must be positive")
+    return _log_integrand_call(t, p, 0)
+
+
+def log_integrand_d1(t: float, p: EvalPoint) -> float:
+    if t < 0.0:
+        raise DomainError("t must be nonnegative")
+    return _log_integrand_call(t, p, 1)
+
+
+def log_integrand_d2(t: float, p: EvalPoint) -> float:
+    if t < 0.0:
+        raise DomainError("t must be nonnegative")
+    return _log_integrand_call(t, p, 2)
+
+
+def fixed_window_log_bessel_k(x: float, nu: float,
+                              cfg: QuadratureConfig = DEFAULT_CONFIG,
+                              bins: int | None = None) -> float:
+    """Raw fixed-window log K with no threshold guard.
+
+    The bound audit and the pure-integral accuracy study deliberately apply
+    this below the series threshold.
+    """
+    if x <= 0.0:
+        raise DomainError("x must be positive")
+    b = cfg.bins if bins is None else int(bins)
+    return _scalar_logk(x, nu, cfg, _lib.ROUTE_INTEGRAL, bins=b)
+
+
+def bessel_k_integral(p: EvalPoint, cfg: QuadratureConfig = DEFAULT_CONFIG) -> BesselResult:
+    """Integral path over the fixed window [t_lower, t_upper]."""
+    if p.x < cfg.small_x_threshold:
+        raise DomainError(
+            f"integral path needs x >= {cfg.small_x_threshold:g}, got {p.x!r}")
+    log_k = fixed_window_log_bessel_k(p.x, p.nu, cfg)
+    return _result(log_k, PathTaken.INTEGRAL, p)
+
+
+def bessel_k(p: EvalPoint, cfg: QuadratureConfig = DEFAULT_CONFIG) -> BesselResult:
+    """K_nu(x): series below the threshold, fixed-window quadrature at and
+    above it (the boundary belongs to the integral side)."""
+    if p.x <= 0.0:
+        raise DomainError("x must be positive (r = 0 is handled by the Matern kernel)")
+    if p.x < cfg.small_x_threshold:
+        return bessel_k_series(p, cfg)
+    return bessel_k_integral(p, cfg)

@@ -1,0 +1,374 @@
+// bgk_capi.cpp -- extern "C" boundary of libbesselgp_sm100a.so (include/besselgp_b200.h).
+//
+// Host-side work here is per call, never per element: argument checks, the
+// Matern plan (node tables + Temme constants + u-bucket LUT, i.e. the restated
+// caller of kernels.matern_tile, kernels.py:343-345 / SPEC.md:306-332) and
+// the task-grid arithmetic of the three Matern layouts.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include <cuda_runtime.h>
+
+#include "bgk_internal.h"
+
+namespace {
+thread_local char g_err[512] = "";
+std::atomic<long long> g_launches{0};
+
+constexpr double kLn2 = 0.6931471805599453;  // kernels.py:16
+
+double log_cosh_host(double z) {  // kernels.py:43-49, glibc libm like numba
+  z = std::fabs(z);
+  if (z < 25.0) return std::log(std::cosh(z));
+  return z - kLn2 + std::log1p(std::exp(-2.0 * z));
+}
+
+double gamma1_host(double mu) {  // kernels.py:219-227
+  static const double G[12] = {
+      0.57721566490153286061,   -0.042002635034095235529, -0.042197734555544336748,
+      0.0072189432466630995424, -0.00021524167411495097282, -2.0134854780788238656e-05,
+      1.1330272319816958824e-06, 6.1160951044814158179e-09, -1.1812745704870201446e-09,
+      7.782263439905071254e-12,  5.100370287454475979e-13,  -5.3481225394230179824e-15};
+  double acc = 0.0, mu2 = mu * mu, p = 1.0;
+  for (int i = 0; i < 12; ++i) {
+    acc += G[i] * p;
+    p *= mu2;
+  }
+  return -acc;
+}
+
+// Bucket key of a positive double: its top 16 bits (sign, exponent, 4 mantissa
+// bits) -> 16 log-spaced buckets per octave.  The device computes the same
+// key with (__double2hiint(u) >> 16).
+int key_of(double u) {
+  uint64_t b;
+  std::memcpy(&b, &u, 8);
+  return (int)(b >> 48);
+}
+double u_of_key(int key) {
+  uint64_t b = (uint64_t)(uint32_t)key << 48;
+  double u;
+  std::memcpy(&u, &b, 8);
+  return u;
+}
+
+struct Window {
+  int m, lo, hi;
+};
+
+// Exact reference window at u: grid argmax m* (first max, kernels.py:363-369)
+// and every node with g_k - g_{m*} > -50 (the reference keeps > -46).
+Window window_at(const bgk_matern_plan &P, double u) {
+  const int nn = P.nnodes;
+  double gmax = -INFINITY;
+  int ms = 0;
+  for (int k = 0; k < nn; ++k) {
+    double g = P.a[k] - u * P.c[k];
+    if (g > gmax) {
+      gmax = g;
+      ms = k;
+    }
+  }
+  Window w{ms, ms, ms};
+  for (int k = 0; k < nn; ++k) {
+    double g = P.a[k] - u * P.c[k];
+    if (g - gmax > -50.0) {
+      if (k < w.lo) w.lo = k;
+      if (k > w.hi) w.hi = k;
+    }
+  }
+  return w;
+}
+
+// Fill plan->lut; sets plan->fast = 0 when a safe LUT cannot be built.
+void build_lut(bgk_matern_plan &P) {
+  P.fast = 0;
+  P.nbuckets = 1;
+  P.key_base = 0;
+  P.lut[0] = 0;
+  const double thr = P.small_x_threshold;
+  if (!(thr > 0.0) || !std::isfinite(thr) || P.nnodes < 2) return;
+  for (int k = 0; k < P.nnodes; ++k)
+    if (!std::isfinite(P.c[k]) || !std::isfinite(P.a[k])) return;
+  const int kb = key_of(thr);
+  // Extend the bucket range until the window at a bucket's lower edge is the
+  // anchor alone; every larger u then shares that single-node window.
+  int kt = std::max(key_of(4096.0), key_of(64.0 * P.nu * P.nu));
+  kt = std::max(kt, kb + 1);
+  for (;;) {
+    Window w = window_at(P, u_of_key(kt));
+    if (w.lo == w.hi) {
+      Window w2 = window_at(P, u_of_key(kt) * 1e6);
+      if (w2.m == w.m) break;
+    }
+    ++kt;
+    if (kt - kb + 1 > BGK_MATERN_MAX_BUCKETS) return;
+  }
+  const int nb = kt - kb + 1;
+  if (nb > BGK_MATERN_MAX_BUCKETS) return;
+  const int S = 9;  // samples per bucket (endpoints + 7 interior, geometric)
+  for (int b = 0; b < nb; ++b) {
+    const double ulo = (b == 0) ? thr : u_of_key(kb + b);
+    const bool last = (b == nb - 1);
+    const double uhi = last ? ulo : std::nextafter(u_of_key(kb + b + 1), 0.0);
+    const double umid = std::sqrt(ulo * uhi);
+    const int anchor = window_at(P, umid).m;
+    int lo = anchor, hi = anchor;
+    for (int s = 0; s < S; ++s) {
+      const double u = (s == 0) ? ulo : (s == S - 1) ? uhi : ulo * std::pow(uhi / ulo, (double)s / (S - 1));
+      Window w = window_at(P, u);
+      lo = std::min(lo, w.lo);
+      hi = std::max(hi, w.hi);
+    }
+    // y_k(u) = g_k(u) - g_anchor(u) is linear in u: bound it at the endpoints so
+    // the table exp never sees |y| beyond its range and never overflows.
+    for (int e = 0; e < 2; ++e) {
+      const double u = e ? uhi : ulo;
+      const double ga = P.a[anchor] - u * P.c[anchor];
+      for (int k = lo; k <= hi; ++k) {
+        const double y = (P.aw[k] - u * P.c[k]) - ga;
+        if (!(y > -700.0 && y < 30.0)) return;
+      }
+    }
+    if (last && lo != hi) return;
+    P.lut[b] = (uint32_t)anchor | ((uint32_t)lo << 10) | ((uint32_t)hi << 20);
+  }
+  P.nbuckets = nb;
+  P.key_base = kb;
+  P.fast = 1;
+}
+
+int check_cfg(const bgk_config *cfg) {
+  if (!cfg) {
+    bgk_set_error("cfg is NULL");
+    return BGK_ERR_INVALID;
+  }
+  if (!(cfg->t_upper > cfg->t_lower) || !std::isfinite(cfg->t_lower) ||
+      !std::isfinite(cfg->t_upper) || cfg->bins < 1 || cfg->series_cap < 0) {
+    bgk_set_error("invalid bgk_config (t_lower=%g t_upper=%g bins=%lld cap=%lld)",
+                  cfg->t_lower, cfg->t_upper, (long long)cfg->bins,
+                  (long long)cfg->series_cap);
+    return BGK_ERR_INVALID;
+  }
+  return BGK_OK;
+}
+
+int check_plan(const bgk_matern_plan *plan) {
+  if (!plan || plan->abi != BGK_ABI_VERSION || plan->nnodes < 1 ||
+      plan->nnodes > BGK_MATERN_MAX_NODES || plan->nbuckets < 1 ||
+      plan->nbuckets > BGK_MATERN_MAX_BUCKETS) {
+    bgk_set_error("invalid or uninitialised bgk_matern_plan");
+    return BGK_ERR_INVALID;
+  }
+  return BGK_OK;
+}
+}  // namespace
+
+void bgk_set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int bgk_check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    bgk_set_error("%s: %s", what, cudaGetErrorString(e));
+    return BGK_ERR_CUDA;
+  }
+  return BGK_OK;
+}
+
+void bgk_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" {
+
+const char *bgk_last_error(void) { return g_err; }
+int bgk_abi_version(void) { return BGK_ABI_VERSION; }
+int64_t bgk_launch_count(void) { return g_launches.load(); }
+size_t bgk_matern_plan_size(void) { return sizeof(bgk_matern_plan); }
+
+int bgk_besselk_batch(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
+                      int route, double *log_k, double *k, uint8_t *path, void *stream) {
+  if (int rc = check_cfg(cfg)) return rc;
+  if (n < 0 || (n > 0 && (!x || !nu || !log_k)) || route < 0 || route > 2) {
+    bgk_set_error("bgk_besselk_batch: bad arguments (n=%lld route=%d)", (long long)n, route);
+    return BGK_ERR_INVALID;
+  }
+  return bgk_launch_besselk(x, nu, n, cfg, route, log_k, k, path, (cudaStream_t)stream);
+}
+
+int bgk_temme_sums_batch(const double *x, const double *mu, int64_t n, const bgk_config *cfg,
+                         double *s0, double *s1, int64_t *terms, void *stream) {
+  if (int rc = check_cfg(cfg)) return rc;
+  if (n < 0 || (n > 0 && (!x || !mu || !s0 || !s1))) {
+    bgk_set_error("bgk_temme_sums_batch: bad arguments");
+    return BGK_ERR_INVALID;
+  }
+  return bgk_launch_temme_sums(x, mu, n, cfg, s0, s1, terms, (cudaStream_t)stream);
+}
+
+int bgk_log_integrand_batch(const double *t, const double *x, const double *nu, int64_t n,
+                            int order, double *out, void *stream) {
+  if (n < 0 || order < 0 || order > 2 || (n > 0 && (!t || !x || !nu || !out))) {
+    bgk_set_error("bgk_log_integrand_batch: bad arguments");
+    return BGK_ERR_INVALID;
+  }
+  return bgk_launch_log_integrand(t, x, nu, n, order, out, (cudaStream_t)stream);
+}
+
+int bgk_matern_plan_init_tables(bgk_matern_plan *plan, double sigma_sq, double beta, double nu,
+                                double log_prefactor, const double *c_nodes,
+                                const double *a_nodes, int64_t nnodes, double h,
+                                double small_x_threshold, double eps_machine,
+                                int64_t series_cap) {
+  if (!plan || !c_nodes || !a_nodes) {
+    bgk_set_error("bgk_matern_plan_init_tables: NULL argument");
+    return BGK_ERR_INVALID;
+  }
+  if (nnodes < 2 || nnodes > BGK_MATERN_MAX_NODES) {
+    bgk_set_error("bgk_matern_plan_init_tables: nnodes=%lld outside [2, %d]",
+                  (long long)nnodes, BGK_MATERN_MAX_NODES);
+    return BGK_ERR_UNSUPPORTED;
+  }
+  std::memset(plan, 0, sizeof(*plan));
+  bgk_matern_plan &P = *plan;
+  P.abi = BGK_ABI_VERSION;
+  P.nnodes = (int32_t)nnodes;
+  P.sigma_sq = sigma_sq;
+  P.beta = beta;
+  P.nu = nu;
+  P.log_prefactor = log_prefactor;
+  P.h = h;
+  P.small_x_threshold = small_x_threshold;
+  P.eps_machine = eps_machine;
+  P.series_cap = series_cap;
+  const int b = (int)nnodes - 1;
+  for (int k = 0; k < nnodes; ++k) {
+    P.c[k] = c_nodes[k];
+    P.a[k] = a_nodes[k];
+    // trapezoid weight 1/2 at both ends (kernels.py:375) folded into the exponent
+    P.aw[k] = (k == 0 || k == b) ? a_nodes[k] - kLn2 : a_nodes[k];
+  }
+  // nu-only Temme constants (kernels.py:240-252, 281-282)
+  P.m_steps = (int32_t)std::floor(nu + 0.5);
+  P.mu = nu - (double)P.m_steps;
+  P.gam1 = gamma1_host(P.mu);
+  P.gamma_1m_mu = std::tgamma(1.0 - P.mu);
+  P.gamma_1p_mu = std::tgamma(1.0 + P.mu);
+  P.gam2 = 0.5 * (1.0 / P.gamma_1m_mu + 1.0 / P.gamma_1p_mu);
+  P.fact = (std::fabs(P.mu) < 1e-10) ? 1.0 : P.mu * M_PI / std::sin(P.mu * M_PI);
+  build_lut(P);
+  return BGK_OK;
+}
+
+int bgk_matern_plan_init(bgk_matern_plan *plan, double sigma_sq, double beta, double nu,
+                         const bgk_config *cfg) {
+  if (int rc = check_cfg(cfg)) return rc;
+  if (cfg->bins + 1 > BGK_MATERN_MAX_NODES) {
+    bgk_set_error("bgk_matern_plan_init: bins=%lld exceeds %d", (long long)cfg->bins,
+                  BGK_MATERN_MAX_NODES - 1);
+    return BGK_ERR_UNSUPPORTED;
+  }
+  const int64_t nn = cfg->bins + 1;
+  double c[BGK_MATERN_MAX_NODES], a[BGK_MATERN_MAX_NODES];
+  // restated caller (kernels.py:343-345): h = (t1-t0)/b, t_m = t0 + m h
+  const double h = (cfg->t_upper - cfg->t_lower) / (double)cfg->bins;
+  for (int64_t m = 0; m < nn; ++m) {
+    const double t = cfg->t_lower + (double)m * h;
+    c[m] = std::cosh(t);
+    a[m] = log_cosh_host(nu * t);
+  }
+  // log(sigma^2 2^(1-nu) / Gamma(nu))
+  const double lp = std::log(sigma_sq) - (nu - 1.0) * kLn2 - std::lgamma(nu);
+  return bgk_matern_plan_init_tables(plan, sigma_sq, beta, nu, lp, c, a, nn, h,
+                                     cfg->small_x_threshold, cfg->eps_machine,
+                                     cfg->series_cap);
+}
+
+int bgk_matern_tile(const bgk_matern_plan *plan, const double *rx, const double *ry, int64_t m,
+                    const double *cx, const double *cy, int64_t n, double *out, int64_t ld,
+                    int layout, void *stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (m < 0 || n < 0 || (layout != BGK_LAYOUT_ROW_MAJOR && layout != BGK_LAYOUT_COL_MAJOR)) {
+    bgk_set_error("bgk_matern_tile: bad sizes or layout");
+    return BGK_ERR_INVALID;
+  }
+  if (m == 0 || n == 0) return BGK_OK;
+  if (!rx || !ry || !cx || !cy || !out || ld < (layout == BGK_LAYOUT_ROW_MAJOR ? n : m)) {
+    bgk_set_error("bgk_matern_tile: NULL pointer or ld too small");
+    return BGK_ERR_INVALID;
+  }
+  BgkMaternArgs A{};
+  A.rx = rx; A.ry = ry; A.cx = cx; A.cy = cy; A.out = out;
+  A.m = m; A.n = n; A.ld = ld; A.layout = layout;
+  A.ntasks = ((m + 63) / 64) * ((n + 63) / 64);
+  return bgk_launch_matern(plan, A, BGK_MODE_TILE, (cudaStream_t)stream);
+}
+
+int bgk_matern_covariance(const bgk_matern_plan *plan, const double *lx, const double *ly,
+                          int64_t N, int64_t row_begin, int64_t row_end, double *out, int64_t ld,
+                          int layout, void *stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (N < 0 || row_begin < 0 || row_end > N || row_begin > row_end ||
+      (layout != BGK_LAYOUT_ROW_MAJOR && layout != BGK_LAYOUT_COL_MAJOR)) {
+    bgk_set_error("bgk_matern_covariance: bad N/rows/layout");
+    return BGK_ERR_INVALID;
+  }
+  const int64_t rows = row_end - row_begin;
+  if (rows == 0 || N == 0) return BGK_OK;
+  if (!lx || !ly || !out || ld < (layout == BGK_LAYOUT_ROW_MAJOR ? N : rows)) {
+    bgk_set_error("bgk_matern_covariance: NULL pointer or ld too small");
+    return BGK_ERR_INVALID;
+  }
+  BgkMaternArgs A{};
+  A.rx = lx; A.ry = ly; A.cx = lx; A.cy = ly; A.out = out;
+  A.m = N; A.n = N; A.ld = ld; A.layout = layout;
+  A.row0 = row_begin; A.row1 = row_end;
+  A.nTr = (rows + 63) / 64;
+  A.nL = (row_begin + 63) / 64;
+  A.nR = (N - row_end + 63) / 64;
+  A.nD = A.nTr * (A.nTr + 1) / 2;
+  A.ntasks = A.nTr * A.nL + A.nD + A.nTr * A.nR;
+  if (A.ntasks > 0x7fffffffLL) {
+    bgk_set_error("bgk_matern_covariance: %lld tiles exceed one launch; shard the rows",
+                  (long long)A.ntasks);
+    return BGK_ERR_UNSUPPORTED;
+  }
+  return bgk_launch_matern(plan, A, BGK_MODE_COV, (cudaStream_t)stream);
+}
+
+int bgk_matern_lower_tiles(const bgk_matern_plan *plan, const double *lx, const double *ly,
+                           int64_t N, int64_t tile_size, int64_t tile_begin, int64_t tile_end,
+                           double *out, void *stream) {
+  if (int rc = check_plan(plan)) return rc;
+  const int64_t T = (N + tile_size - 1) / (tile_size > 0 ? tile_size : 1);
+  const int64_t total = T * (T + 1) / 2;
+  if (N < 0 || tile_size < 1 || tile_begin < 0 || tile_end > total || tile_begin > tile_end) {
+    bgk_set_error("bgk_matern_lower_tiles: bad N/tile_size/tile range");
+    return BGK_ERR_INVALID;
+  }
+  if (tile_end == tile_begin || N == 0) return BGK_OK;
+  if (!lx || !ly || !out) {
+    bgk_set_error("bgk_matern_lower_tiles: NULL pointer");
+    return BGK_ERR_INVALID;
+  }
+  BgkMaternArgs A{};
+  A.rx = lx; A.ry = ly; A.cx = lx; A.cy = ly; A.out = out;
+  A.m = N; A.n = N; A.ts = tile_size;
+  A.tile0 = tile_begin; A.tile1 = tile_end;
+  A.sub = (tile_size + 63) / 64;
+  A.ntasks = (tile_end - tile_begin) * A.sub * A.sub;
+  if (A.ntasks > 0x7fffffffLL) {
+    bgk_set_error("bgk_matern_lower_tiles: %lld sub-tiles exceed one launch; split the range",
+                  (long long)A.ntasks);
+    return BGK_ERR_UNSUPPORTED;
+  }
+  return bgk_launch_matern(plan, A, BGK_MODE_LOWER, (cudaStream_t)stream);
+}
+
+}  // extern "C"

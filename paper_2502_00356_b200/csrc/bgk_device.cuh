@@ -1,0 +1,234 @@
+// bgk_device.cuh -- device math shared by the BesselK and Matern kernels (sm_100a).
+//
+// Everything here is FP64.  The hot loops are bound by the FP64 pipe (64 lanes
+// per SM per clock on B200), so the per-node exponential is a table-driven
+// 2^(j/64) * poly5 scheme (10 FP64 ops, 2-3 ulp) instead of libdevice exp
+// (15 ops + range checks); rarely-hit paths (Temme series, out-of-range
+// parameters) keep libdevice for robustness.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+namespace bgk {
+
+constexpr double kLn2 = 0.6931471805599453;  // kernels.py:16
+constexpr double kPi = 3.141592653589793;
+
+// 2^(j/64), j = 0..63, correctly rounded (generated with mpmath, 200 bits).
+__device__ __constant__ double kExp2Tab64[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
+};
+
+// Copy the exp table into shared memory (call from all threads, then sync).
+__device__ __forceinline__ void load_exp_tab(double *tab) {
+  for (int j = threadIdx.x; j < 64; j += blockDim.x) tab[j] = kExp2Tab64[j];
+}
+
+// e^y for y in [-707, 709]: y = (64 n + j) ln2/64 + r, |r| <= ln2/128,
+// e^y = 2^n * 2^(j/64) * poly5(r).  Cody-Waite two-constant reduction; the
+// degree-5 Taylor tail is r^6/720 < 3.5e-17.  Outside the range the result is
+// garbage (callers clamp or mask).  10 FP64-pipe ops + 1 LDS + 3 integer ops.
+__device__ __forceinline__ double exp_tab(double y, const double *__restrict__ tab) {
+  const double kMagic = 0x1.8p52;
+  const double kInvL = 0x1.71547652b82fep+6;  // 64/ln2
+  const double kL1 = 0x1.62e42fefa39efp-7;    // ln2/64 (hi)
+  const double kL2 = 0x1.abc9e3b39803fp-62;   // ln2/64 (lo)
+  double t = fma(y, kInvL, kMagic);
+  double nd = t - kMagic;
+  int n = __double2loint(t);
+  double r = fma(nd, -kL1, y);
+  r = fma(nd, -kL2, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  double e = tab[n & 63] * p;
+  int hi = __double2hiint(e) + ((n >> 6) << 20);
+  return __hiloint2double(hi, __double2loint(e));
+}
+
+// Full-range e^y (any finite y, inf/0 on overflow/underflow like exp()).
+__device__ __forceinline__ double exp_full(double y, const double *__restrict__ tab) {
+  return (fabs(y) < 700.0) ? exp_tab(y, tab) : exp(y);
+}
+
+// kernels.py:43-49
+__device__ __forceinline__ double log_cosh(double z) {
+  z = fabs(z);
+  if (z < 25.0) return log(cosh(z));
+  return z - kLn2 + log1p(exp(-2.0 * z));
+}
+
+// ---------------------------------------------------------------------------------
+// Temme small-argument series (kernels.py:219-293).  Same formulas and stop rule
+// as the reference; libdevice tgamma/sin/sinh/cosh/exp/log (<= 2 ulp).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ double gamma1(double mu) {  // kernels.py:219-227
+  const double G[12] = {
+      0.57721566490153286061,   -0.042002635034095235529, -0.042197734555544336748,
+      0.0072189432466630995424, -0.00021524167411495097282, -2.0134854780788238656e-05,
+      1.1330272319816958824e-06, 6.1160951044814158179e-09, -1.1812745704870201446e-09,
+      7.782263439905071254e-12,  5.100370287454475979e-13,  -5.3481225394230179824e-15};
+  double acc = 0.0, mu2 = mu * mu, p = 1.0;
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    acc += G[i] * p;
+    p *= mu2;
+  }
+  return -acc;
+}
+
+// The nu-only part of temme_sums (kernels.py:240-245, 251-252).
+struct TemmeConst {
+  double mu, gam1, gam2, fact, g1p, g1m;
+  int m_steps;
+};
+
+__device__ __forceinline__ TemmeConst temme_const(double nu) {
+  TemmeConst T;
+  T.m_steps = (int)floor(nu + 0.5);  // kernels.py:281
+  T.mu = nu - (double)T.m_steps;
+  T.gam1 = gamma1(T.mu);
+  T.g1m = tgamma(1.0 - T.mu);
+  T.g1p = tgamma(1.0 + T.mu);
+  T.gam2 = 0.5 * (1.0 / T.g1m + 1.0 / T.g1p);
+  T.fact = (fabs(T.mu) < 1e-10) ? 1.0 : T.mu * kPi / sin(T.mu * kPi);
+  return T;
+}
+
+// kernels.py:230-270 with the nu-only constants supplied.  Returns terms.
+__device__ __forceinline__ long long temme_sums_c(double x, const TemmeConst &T, double eps,
+                                                  long long cap, double &s0o, double &s1o) {
+  const double mu = T.mu;
+  double d = log(2.0 / x);
+  double sigma = mu * d;
+  double sh = (sigma == 0.0) ? 1.0 : sinh(sigma) / sigma;
+  double f = T.fact * (cosh(sigma) * T.gam1 + T.gam2 * sh * d);
+  double p = 0.5 * exp(sigma) * T.g1p;
+  double q = 0.5 * exp(-sigma) * T.g1m;
+  double c = 1.0, s0 = f, s1 = p, x2_4 = 0.25 * x * x;
+  long long terms = 1;
+  for (long long k = 1; k < cap + 1; ++k) {
+    double kd = (double)k;
+    f = (kd * f + p + q) / (kd * kd - mu * mu);
+    p /= (kd - mu);
+    q /= (kd + mu);
+    c *= x2_4 / kd;
+    double del0 = c * f;
+    double del1 = c * (p - kd * f);
+    s0 += del0;
+    s1 += del1;
+    terms = k + 1;
+    if (fabs(del0) < eps * fabs(s0) && fabs(del1) < eps * fabs(s1)) break;
+  }
+  s0o = s0;
+  s1o = s1;
+  return terms;
+}
+
+// kernels.py:273-293: ln K_nu(x) via Temme + log-space forward recurrence.
+__device__ __forceinline__ double temme_series_log_c(double x, const TemmeConst &T, double eps,
+                                                     long long cap) {
+  double s0, s1;
+  temme_sums_c(x, T, eps, cap, s0, s1);
+  double l_prev = log(s0);
+  if (T.m_steps == 0) return l_prev;
+  double l_cur = kLn2 - log(x) + log(s1);
+  for (int k = 1; k < T.m_steps; ++k) {
+    double eta = T.mu + (double)k;
+    double l_next = l_cur + log(2.0 * eta / x + exp(l_prev - l_cur));
+    l_prev = l_cur;
+    l_cur = l_next;
+  }
+  return l_cur;
+}
+
+// ---------------------------------------------------------------------------------
+// Reference-faithful fixed-window quadrature (kernels.py:112-216): grid argmax,
+// hyperbolic-identity node exponents, walk with the -46 break, Kahan, rebase.
+// Used only where the fast kernels' preconditions fail (t_lower < 0, nu*t so
+// large that e^(nu t) overflows, very large bin counts).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ double node_exponent_ref(double anu, double x, double dt,
+                                                    double z_star, double lc_star,
+                                                    double ch_star, double ss, double cs) {
+  double z_m = z_star + anu * dt;
+  double da;
+  if (z_m >= 30.0 && z_star >= 30.0)
+    da = anu * dt;
+  else if (z_m < 25.0 && z_star < 25.0)
+    da = log(cosh(z_m) / ch_star);
+  else
+    da = log_cosh(z_m) - lc_star;
+  double sh = sinh(0.5 * dt);
+  double ch = cosh(0.5 * dt);
+  double db = 2.0 * x * (ss * ch + cs * sh) * sh;
+  return da - db;
+}
+
+__device__ __noinline__ static double fixed_window_log_ref(double x, double nu, double t0, double t1, long long bins) {
+  const double h = (t1 - t0) / (double)bins;
+  // grid_peak_index, kernels.py:112-123
+  double best = -INFINITY;
+  long long m_star = 0;
+  for (long long m = 0; m < bins + 1; ++m) {
+    double t = t0 + (double)m * h;
+    double g = log_cosh(nu * t) - x * cosh(t);
+    if (g > best) {
+      best = g;
+      m_star = m;
+    }
+  }
+  // window_lse, kernels.py:154-209
+  double anu = fabs(nu);
+  double t_star = t0 + (double)m_star * h;
+  double z_star = anu * t_star;
+  double lc_star = log_cosh(z_star);
+  double ch_star = (z_star < 25.0) ? cosh(z_star) : INFINITY;
+  double ss = sinh(t_star), cs = cosh(t_star);
+  double acc = (0 < m_star && m_star < bins) ? 1.0 : 0.5;
+  double comp = 0.0;
+  for (int direction = 0; direction < 2; ++direction) {
+    double sign = (direction == 0) ? 1.0 : -1.0;
+    long long span = (direction == 0) ? (bins - m_star) : m_star;
+    for (long long k = 1; k < span + 1; ++k) {
+      double dt = sign * ((double)k * h);
+      double dg = node_exponent_ref(anu, x, dt, z_star, lc_star, ch_star, ss, cs);
+      if (dg <= -46.0) break;
+      long long m = m_star + ((direction == 0) ? k : -k);
+      double w = (m == 0 || m == bins) ? 0.5 : 1.0;
+      double y = w * exp(dg) - comp;
+      double t_acc = acc + y;
+      comp = (t_acc - acc) - y;
+      acc = t_acc;
+    }
+  }
+  double t_hat = (anu * anu <= x) ? 0.0 : asinh(anu / x);
+  double z_hat = anu * t_hat;
+  double shift = log_cosh(z_hat) - x * cosh(t_hat);
+  double dt_sh = t_star - t_hat;
+  double da_sh = (z_star >= 30.0 && z_hat >= 30.0) ? anu * dt_sh : lc_star - log_cosh(z_hat);
+  double sh = sinh(0.5 * dt_sh);
+  double db_sh = 2.0 * x * (sinh(t_hat) * cosh(0.5 * dt_sh) + cosh(t_hat) * sh) * sh;
+  return shift + ((da_sh - db_sh) + log(h * acc));
+}
+
+}  // namespace bgk

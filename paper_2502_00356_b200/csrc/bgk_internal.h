@@ -1,0 +1,43 @@
+// bgk_internal.h -- declarations shared between the CUDA launchers and the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/besselgp_b200.h"
+
+// error/launch bookkeeping (bgk_capi.cpp)
+void bgk_set_error(const char *fmt, ...);
+int bgk_check_launch(const char *what);
+void bgk_note_launch();
+
+// launchers
+int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
+                       int route, double *log_k, double *k, uint8_t *path, cudaStream_t stream);
+int bgk_launch_temme_sums(const double *x, const double *mu, int64_t n, const bgk_config *cfg,
+                          double *s0, double *s1, int64_t *terms, cudaStream_t stream);
+int bgk_launch_log_integrand(const double *t, const double *x, const double *nu, int64_t n,
+                             int order, double *out, cudaStream_t stream);
+
+// Matern launch descriptor (one of three task decoders)
+enum BgkMaternMode { BGK_MODE_TILE = 0, BGK_MODE_COV = 1, BGK_MODE_LOWER = 2 };
+
+struct BgkMaternArgs {
+  const double *rx, *ry;  // row locations (COV/LOWER: all N locations)
+  const double *cx, *cy;  // column locations
+  double *out;
+  long long m, n;         // TILE: rows/cols; COV/LOWER: N, N
+  long long ld;           // TILE/COV leading dimension
+  int layout;             // BGK_LAYOUT_*
+  long long row0, row1;   // COV shard
+  long long ts;           // LOWER storage tile size
+  long long tile0, tile1; // LOWER tile range
+  long long ntasks;
+  // COV decode helpers
+  long long nTr, nL, nR, nD;
+  // LOWER decode helper
+  long long sub;          // ceil(ts/64)
+};
+
+int bgk_launch_matern(const bgk_matern_plan *plan, BgkMaternArgs &args, int mode,
+                      cudaStream_t stream);
