@@ -136,6 +136,41 @@ void build_lut(bgk_matern_plan &P) {
     if (last && lo != hi) return;
     P.lut[b] = (uint32_t)anchor | ((uint32_t)lo << 10) | ((uint32_t)hi << 20);
   }
+  // The kernel reads a sorted warp's common/union window from its first and
+  // last lanes, which needs lo and hi non-increasing in u.  They are by
+  // construction (the peak moves left and narrows as u grows); enforce it by
+  // widening (prefix-min of lo, suffix-max of hi) and re-check the y bounds.
+  for (int b = 1; b < nb; ++b) {
+    const uint32_t prev = P.lut[b - 1], cur = P.lut[b];
+    const uint32_t lo = std::min((cur >> 10) & 1023, (prev >> 10) & 1023);
+    P.lut[b] = (cur & 1023) | (lo << 10) | (cur & (1023u << 20));
+  }
+  for (int b = nb - 2; b >= 0; --b) {
+    const uint32_t next = P.lut[b + 1], cur = P.lut[b];
+    const uint32_t hi = std::max(cur >> 20, next >> 20);
+    P.lut[b] = (cur & ((1u << 20) - 1)) | (hi << 20);
+  }
+  for (int b = 0; b < nb; ++b) {
+    const double ulo = (b == 0) ? thr : u_of_key(kb + b);
+    const double uhi = (b == nb - 1) ? ulo : std::nextafter(u_of_key(kb + b + 1), 0.0);
+    const int anchor = P.lut[b] & 1023, lo = (P.lut[b] >> 10) & 1023, hi = P.lut[b] >> 20;
+    if (b == nb - 1 && lo != hi) return;
+    for (int e = 0; e < 2; ++e) {
+      const double u = e ? uhi : ulo;
+      const double ga = P.a[anchor] - u * P.c[anchor];
+      for (int k = lo; k <= hi; ++k) {
+        const double y = (P.aw[k] - u * P.c[k]) - ga;
+        if (!(y > -700.0 && y < 30.0)) return;
+      }
+    }
+  }
+  int amin = BGK_MATERN_MAX_NODES, amax = 0;
+  for (int b = 0; b < nb; ++b) {
+    amin = std::min(amin, (int)(P.lut[b] & 1023));
+    amax = std::max(amax, (int)(P.lut[b] & 1023));
+  }
+  P.anchor_min = amin;
+  P.anchor_max = amax;
   P.nbuckets = nb;
   P.key_base = kb;
   P.fast = 1;

@@ -11,6 +11,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "bgk_tables.cuh"
+
 namespace bgk {
 
 constexpr double kLn2 = 0.6931471805599453;  // kernels.py:16
@@ -68,6 +70,86 @@ __device__ __forceinline__ double exp_tab(double y, const double *__restrict__ t
 // Full-range e^y (any finite y, inf/0 on overflow/underflow like exp()).
 __device__ __forceinline__ double exp_full(double y, const double *__restrict__ tab) {
   return (fabs(y) < 700.0) ? exp_tab(y, tab) : exp(y);
+}
+
+// ---------------------------------------------------------------------------------
+// 128-entry table exp / log.  Coefficients live in __constant__ memory so DFMA
+// takes them as constant-bank operands (no per-iteration register moves).
+// ---------------------------------------------------------------------------------
+__device__ __constant__ double kExpK[8] = {
+    0x1.71547652b82fep+7,   // 0: 128/ln2
+    0x1.62e42fefa39efp-8,   // 1: ln2/128 (hi)
+    0x1.abc9e3b39803fp-63,  // 2: ln2/128 (lo)
+    1.0 / 24.0,             // 3
+    1.0 / 6.0,              // 4
+    1.0 / 120.0,            // 5
+    0x1.8p52,               // 6: round-to-int magic
+    0.0};
+__device__ __constant__ double kLogK[8] = {
+    0.2, -1.0 / 6.0, -0.25, 1.0 / 3.0, -0.5,
+    0x1.62e4200000000p-1,   // 5: ln2 hi (21 bits: e * hi is exact)
+    0x1.fdf473de6af28p-22,  // 6: ln2 lo
+    0.0};
+
+// Copy the 128-entry exp table and the log tables into shared memory.
+__device__ __forceinline__ void load_tables128(double *exp128, double *invc, double *logc) {
+  for (int j = threadIdx.x; j < 128; j += blockDim.x) {
+    exp128[j] = kExp2Tab128[j];
+    invc[j] = kInvC128[j];
+    logc[j] = kLogC128[j];
+  }
+}
+
+// e^y for a quadrature node, y in (-707, 700): 128-entry table, degree-4
+// polynomial on |r| <= ln2/256 (truncation 1.2e-15) and a one-constant
+// reduction (error |y| * 1.2e-16, harmless because the term is e^y).
+// 7 FP64 ops + LDS + 4 integer ops.
+__device__ __forceinline__ double exp_node(double y, const double *__restrict__ t128) {
+  const double t = fma(y, kExpK[0], kExpK[6]);
+  const double nd = t - kExpK[6];
+  const int n = __double2loint(t);
+  const double r = fma(nd, -kExpK[1], y);
+  double p = fma(r, kExpK[3], kExpK[4]);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double e = t128[n & 127] * p;
+  return __hiloint2double(__double2hiint(e) + ((n >> 7) << 20), __double2loint(e));
+}
+
+// e^y to ~2 ulp for |y| < 700 (two-constant reduction, degree 5).
+__device__ __forceinline__ double exp_acc(double y, const double *__restrict__ t128) {
+  const double t = fma(y, kExpK[0], kExpK[6]);
+  const double nd = t - kExpK[6];
+  const int n = __double2loint(t);
+  double r = fma(nd, -kExpK[1], y);
+  r = fma(nd, -kExpK[2], r);
+  double p = fma(r, kExpK[5], kExpK[3]);
+  p = fma(p, r, kExpK[4]);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double e = t128[n & 127] * p;
+  return __hiloint2double(__double2hiint(e) + ((n >> 7) << 20), __double2loint(e));
+}
+
+// log(x) for positive, normal, finite x: x = 2^e m, m in [1,2), table point
+// c_j = 1 + (j+1/2)/128, f = m/c_j - 1 (|f| <= 1/256), log1p(f) to degree 6.
+// ~11 FP64 ops, <= 1 ulp-ish.
+__device__ __forceinline__ double log_fast(double x, const double *__restrict__ invc,
+                                           const double *__restrict__ logc) {
+  const int hi = __double2hiint(x);
+  const int e = (hi >> 20) - 1023;
+  const int j = (hi >> 13) & 127;
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(x));
+  const double f = fma(m, invc[j], -1.0);
+  double q = fma(f, kLogK[1], kLogK[0]);
+  q = fma(q, f, kLogK[2]);
+  q = fma(q, f, kLogK[3]);
+  q = fma(q, f, kLogK[4]);
+  const double l1p = fma(q, f * f, f);
+  const double ed = (double)e;
+  return fma(ed, kLogK[5], logc[j]) + fma(ed, kLogK[6], l1p);
 }
 
 // kernels.py:43-49
