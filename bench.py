@@ -113,15 +113,6 @@ class Dist:
             self.pg.destroy_process_group()
 
 
-def row_shard(N, world, rank):
-    return N * rank // world, N * (rank + 1) // world
-
-
-def tile_shard(ntiles, world, rank):
-    """Contiguous range of packed lower tiles; tiles are equal work, so equal counts."""
-    return ntiles * rank // world, ntiles * (rank + 1) // world
-
-
 # ---------------------------------------------------------------------------------------
 # clocks (nvidia-smi sampled during the timed region)
 # ---------------------------------------------------------------------------------------
@@ -288,6 +279,7 @@ def run_matern(args, D: Dist) -> dict:
     import paper_2502_00356_b200 as bg
     from paper_2502_00356_b200 import _lib
     from paper_2502_00356_b200.covariance import _cov_launch, _lower_launch, matern_plan
+    from paper_2502_00356_b200.distributed import computed_entries, row_shard, tile_shard
 
     wl = WORKLOADS[args.workload]
     N = wl["N"]
@@ -310,7 +302,7 @@ def run_matern(args, D: Dist) -> dict:
         r0, r1 = row_shard(N, D.world, D.rank)
         out = torch.empty((r1 - r0, N), dtype=torch.float64, device=dev)
         R = r1 - r0
-        computed_local = float(R * (N - R) + R * (R + 1) / 2)
+        computed_local = float(computed_entries(N, r0, r1))
         stored_local = float(R * N)
     stream = torch.cuda.current_stream(dev)
 
@@ -398,7 +390,9 @@ def run_besselk(args, D: Dist) -> dict:
 
     n_total = WORKLOADS["bk"]["n"]
     dev = torch.device("cuda", D.local)
-    i0, i1 = n_total * D.rank // D.world, n_total * (D.rank + 1) // D.world
+    from paper_2502_00356_b200.distributed import batch_shard
+
+    i0, i1 = batch_shard(n_total, D.world, D.rank)
     rng = np.random.default_rng(SEED)
     x = 140.0 * (1.0 - rng.random(n_total))
     nu = 20.0 * (1.0 - rng.random(n_total))
@@ -474,6 +468,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=12.0,
+                    help="seconds of CPU work per reference / cpu_baseline sample")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup raised to the contract minimum of 3")
@@ -581,7 +577,7 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
                                   "device row blocks, D2H of every row (wall clock, max over ranks)"}
         if world == 1 and not args.no_cpu_baseline:
             locs = make_locs(N)
-            c = cpu_matern_sample(N, nus[0], locs)
+            c = cpu_matern_sample(N, nus[0], locs, target_s=args.cpu_sample_s)
             line["cpu_baseline"] = {"value": c["full_job_s"] * len(nus), "unit": "s",
                                     "cores": c["threads"], "kind": "port",
                                     "sample": c["sample"], "cpu": cpu_model()}
@@ -607,7 +603,7 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
             line["e2e"] = {"value": n / r["e2e_s"], "unit": "evals/s",
                            "h2d_bytes_per_step": 16.0 * n, "d2h_bytes_per_step": 17.0 * n}
         if world == 1 and not args.no_cpu_baseline:
-            c = cpu_besselk_sample(r["x"], r["nu"])
+            c = cpu_besselk_sample(r["x"], r["nu"], target_s=args.cpu_sample_s * 2 / 3)
             line["cpu_baseline"] = {"value": c["rate"], "unit": "evals/s", "cores": c["threads"],
                                     "kind": "port", "sample": f"first {c['n']} elements, "
                                     f"{c['t']:.2f} s", "cpu": cpu_model()}
@@ -627,7 +623,7 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
                                         "h2d_bytes_per_step": 16.0 * n2,
                                         "d2h_bytes_per_step": 17.0 * n2}
         if not args.no_cpu_baseline:
-            c = cpu_besselk_sample(sec["x"], sec["nu"])
+            c = cpu_besselk_sample(sec["x"], sec["nu"], target_s=args.cpu_sample_s * 2 / 3)
             line["secondary"]["cpu_baseline"] = {
                 "value": c["rate"], "unit": "evals/s", "cores": c["threads"], "kind": "port",
                 "sample": f"first {c['n']} elements of the same batch, {c['t']:.2f} s"}
@@ -647,7 +643,9 @@ def reference_line(args, world, wl, matern) -> dict:
         for k in range(args.warmup + args.steps):
             tot = 0.0
             for nu in nus:
-                last = cpu_matern_sample(N, nu, locs, target_s=6.0 if k >= args.warmup else 1.0)
+                last = cpu_matern_sample(N, nu, locs, target_s=(args.cpu_sample_s / 2
+                                                                 if k >= args.warmup else
+                                                                 args.cpu_sample_s / 12))
                 tot += last["full_job_s"]
             if k >= args.warmup:
                 per_step.append(tot)
@@ -670,7 +668,7 @@ def reference_line(args, world, wl, matern) -> dict:
     rates = []
     last = None
     for k in range(args.warmup + args.steps):
-        last = cpu_besselk_sample(x, nu, target_s=4.0)
+        last = cpu_besselk_sample(x, nu, target_s=args.cpu_sample_s / 3)
         if k >= args.warmup:
             rates.append(last["rate"])
     v = statistics.median(rates)

@@ -123,6 +123,7 @@ def _stream_handle():
 
 def _to_device(a, device=None):
     """float64 contiguous CUDA tensor view/copy of ``a`` (numpy, list, scalar or tensor)."""
+    _lib.lib()  # BackendUnavailable (not a CPU fallback) when there is no GPU / library
     torch = _torch()
     if isinstance(a, torch.Tensor):
         t = a.to(dtype=torch.float64)

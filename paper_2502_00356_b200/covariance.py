@@ -214,6 +214,7 @@ def _stream():
 
 
 def _dev(a, device=None):
+    _lib.lib()  # BackendUnavailable (not a CPU fallback) when there is no GPU / library
     torch = _torch()
     if isinstance(a, torch.Tensor):
         t = a.to(dtype=torch.float64)
@@ -225,6 +226,7 @@ def _dev(a, device=None):
 
 def _coords(locs):
     """(x, y) float64 CUDA tensors from a LocationSet, an (N,2) array or tensor."""
+    _lib.lib()  # BackendUnavailable (not a CPU fallback) when there is no GPU / library
     torch = _torch()
     if isinstance(locs, LocationSet):
         c = locs.coords
