@@ -117,6 +117,35 @@ __device__ __forceinline__ double exp_node(double y, const double *__restrict__ 
   return __hiloint2double(__double2hiint(e) + ((n >> 7) << 20), __double2loint(e));
 }
 
+// Variant of exp_node on a 16-entry table 2^(j/16) (= every 8th entry of the
+// 128 table): each 8-byte entry owns one shared-memory bank pair, so a warp's
+// lookups never conflict (the 128-entry table costs ~3 wavefronts per
+// half-warp).  Degree-6 polynomial on |r| <= ln2/32 (truncation 4.4e-16),
+// one-constant reduction.  9 FP64 ops + LDS + 4 integer ops.
+__device__ __constant__ double kExp16K[3] = {
+    0x1.71547652b82fep+4,  // 16/ln2
+    0x1.62e42fefa39efp-5,  // ln2/16
+    1.0 / 720.0};
+
+__device__ __forceinline__ void load_exp16(double *t16) {
+  for (int j = threadIdx.x; j < 16; j += blockDim.x) t16[j] = kExp2Tab128[8 * j];
+}
+
+__device__ __forceinline__ double exp_node16(double y, const double *__restrict__ t16) {
+  const double t = fma(y, kExp16K[0], kExpK[6]);
+  const double nd = t - kExpK[6];
+  const int n = __double2loint(t);
+  const double r = fma(nd, -kExp16K[1], y);
+  double p = fma(r, kExp16K[2], kExpK[5]);
+  p = fma(p, r, kExpK[3]);
+  p = fma(p, r, kExpK[4]);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double e = t16[n & 15] * p;
+  return __hiloint2double(__double2hiint(e) + ((n >> 4) << 20), __double2loint(e));
+}
+
 // e^y to ~2 ulp for |y| < 700 (two-constant reduction, degree 5).
 __device__ __forceinline__ double exp_acc(double y, const double *__restrict__ t128) {
   const double t = fma(y, kExpK[0], kExpK[6]);

@@ -33,10 +33,10 @@ struct BgkMaternArgs {
   long long ts;           // LOWER storage tile size
   long long tile0, tile1; // LOWER tile range
   long long ntasks;
-  // COV decode helpers
+  // COV decode helpers (filled by bgk_launch_matern)
   long long nTr, nL, nR, nD;
-  // LOWER decode helper
-  long long sub;          // ceil(ts/64)
+  // LOWER decode helpers (filled by bgk_launch_matern)
+  long long sub, subc;    // sub-tiles per storage tile: rows, cols
 };
 
 int bgk_launch_matern(const bgk_matern_plan *plan, BgkMaternArgs &args, int mode,
