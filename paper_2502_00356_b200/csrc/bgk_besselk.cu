@@ -61,7 +61,7 @@ struct BkArgs {
   int bins;
   int route;
   int table_ok;  // 1: c table fits in shared memory and t0 >= 0 -> fast path allowed
-  uint8_t pred[kXCells * kNuCells];  // predicted max(up, down) walk steps per cell
+  const uint8_t *pred;  // device: predicted max(up, down) walk steps per (x, nu) cell
 };
 
 __host__ __device__ inline int x_cell(double x) {
@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
   __shared__ uint8_t spath[kBkChunk];
   __shared__ int hist[kBuckets + 1];
   __shared__ uint8_t spred[kXCells * kNuCells];
+  __shared__ int s_next;
   double *ctab = smem;  // bins + 1 (only when table_ok)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -160,7 +161,12 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
   if (A.table_ok)
     for (int k = tid; k <= A.bins; k += kBkThreads) ctab[k] = cosh(A.t0 + (double)k * A.h);
   for (int b = tid; b <= kBuckets; b += kBkThreads) hist[b] = 0;
-  for (int c = tid; c < kXCells * kNuCells; c += kBkThreads) spred[c] = A.pred[c];
+  if (A.table_ok) {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(A.pred);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(spred);
+    for (int c = tid; c < kXCells * kNuCells / 4; c += kBkThreads) dst[c] = __ldg(src + c);
+  }
+  if (tid == 0) s_next = 0;
 
   const long long base = (long long)blockIdx.x * kBkChunk;
   const int cnt = (int)min((long long)kBkChunk, A.n - base);
@@ -177,7 +183,8 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
     if (series) return 0;
     const double a = fabs(nu);
     if (!(A.table_ok && a * tmax <= 600.0)) return kBuckets - 1;  // general path: last
-    return 1 + min((int)spred[x_cell(x) * kNuCells + nu_cell(a)], kMaxPred - 1);
+    // longest predicted walks first (they are pulled first in the compute phase)
+    return kMaxPred - min((int)spred[x_cell(x) * kNuCells + nu_cell(a)], kMaxPred - 1);
   };
   for (int e = tid; e < cnt; e += kBkThreads) atomicAdd(&hist[bucket_of(sx[e], snu[e])], 1);
   __syncthreads();
@@ -205,11 +212,13 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
     perm[atomicAdd(&hist[bucket_of(sx[e], snu[e])], 1)] = (uint16_t)e;
   __syncthreads();
 
-  // compute in sorted order; warps take 32-element groups in a snake
+  // compute in sorted order: warps pull 32-element groups from a shared counter,
+  // longest predicted walks first
   const int ngroups = (cnt + 31) >> 5;
-  for (int round = 0; round * 8 < ngroups; ++round) {
-    const int g = round * 8 + ((round & 1) ? 7 - warp : warp);
-    if (g >= ngroups) continue;
+  for (;;) {
+    int g = lane == 0 ? atomicAdd(&s_next, 1) : 0;
+    g = __shfl_sync(0xffffffffu, g, 0);
+    if (g >= ngroups) break;
     const int p = g * 32 + lane;
     if (p >= cnt) continue;
     const int e = perm[p];
@@ -337,14 +346,20 @@ static void build_pred_table(double t0, double t1, int bins, uint8_t *pred) {
 // ---------------------------------------------------------------------------------
 // launchers (called from bgk_capi.cpp)
 // ---------------------------------------------------------------------------------
+// Device copies of the walk-length prediction table, one per (t0, t1, bins), built
+// on the host and uploaded once (3 KB each); kept for the life of the process.
+struct PredEntry {
+  double t0, t1;
+  long long bins;
+  uint8_t *dev;
+};
+
 int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
                        int route, double *log_k, double *k, uint8_t *path, cudaStream_t stream) {
   if (n == 0) return 0;
-  static bgk::BkArgs A;  // large (3 KB table); filled under the lock, launched by value
   static std::mutex mu;
-  static double cached_t0 = NAN, cached_t1 = NAN;
-  static long long cached_bins = -1;
-  std::lock_guard<std::mutex> lock(mu);
+  static std::vector<PredEntry> cache;
+  bgk::BkArgs A;
   A.x = x;
   A.nu = nu;
   A.log_k = log_k;
@@ -361,12 +376,24 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
   A.route = route;
   const int64_t kMaxTable = 16383;  // 128 KB of shared memory
   A.table_ok = (cfg->t_lower >= 0.0 && cfg->bins <= kMaxTable) ? 1 : 0;
-  if (A.table_ok && (cached_t0 != cfg->t_lower || cached_t1 != cfg->t_upper ||
-                     cached_bins != cfg->bins)) {
-    bgk::build_pred_table(cfg->t_lower, cfg->t_upper, (int)cfg->bins, A.pred);
-    cached_t0 = cfg->t_lower;
-    cached_t1 = cfg->t_upper;
-    cached_bins = cfg->bins;
+  A.pred = nullptr;
+  if (A.table_ok) {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const PredEntry &e : cache)
+      if (e.t0 == cfg->t_lower && e.t1 == cfg->t_upper && e.bins == cfg->bins) A.pred = e.dev;
+    if (!A.pred) {
+      std::vector<uint8_t> host(bgk::kXCells * bgk::kNuCells);
+      bgk::build_pred_table(cfg->t_lower, cfg->t_upper, (int)cfg->bins, host.data());
+      uint8_t *dev = nullptr;
+      cudaError_t err = cudaMalloc(&dev, host.size());
+      if (err == cudaSuccess) err = cudaMemcpy(dev, host.data(), host.size(), cudaMemcpyHostToDevice);
+      if (err != cudaSuccess) {
+        bgk_set_error("besselk prediction table upload: %s", cudaGetErrorString(err));
+        return BGK_ERR_CUDA;
+      }
+      cache.push_back({cfg->t_lower, cfg->t_upper, cfg->bins, dev});
+      A.pred = dev;
+    }
   }
   size_t smem = sizeof(double) * (A.table_ok ? (size_t)cfg->bins + 1 : 0);
   static bool attr_set = false;
