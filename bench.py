@@ -61,52 +61,51 @@ def log(*a):
 # ---------------------------------------------------------------------------------------
 
 class Dist:
+    """One process per GPU (torchrun env).  NCCL by default; BGK_BENCH_BACKEND=gloo
+    lets several ranks share one GPU (device = LOCAL_RANK mod device count) to test
+    the N>1 harness on a single-GPU box."""
+
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = os.environ.get("BGK_BENCH_BACKEND", "nccl")
         self.pg = None
+        self.device_index = self.local
 
-    def init(self, backend="nccl"):
+    def init(self):
         import torch
 
+        if torch.cuda.is_available():
+            self.device_index = self.local % torch.cuda.device_count()
+            torch.cuda.set_device(self.device_index)
         if self.world > 1 and self.pg is None:
             import torch.distributed as dist
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            if backend == "nccl":
-                torch.cuda.set_device(self.local)
-            dist.init_process_group(backend)
+            dist.init_process_group(self.backend)
             self.pg = dist
-        elif backend == "nccl":
-            torch.cuda.set_device(self.local)
 
     def barrier(self):
         if self.pg:
-            import torch
-
-            if torch.cuda.is_available():
-                self.pg.barrier(device_ids=[self.local])
+            if self.backend == "nccl":
+                self.pg.barrier(device_ids=[self.device_index])
             else:
                 self.pg.barrier()
 
-    def max(self, v: float) -> float:
-        if not self.pg:
-            return v
+    def _reduce(self, v: float, op) -> float:
         import torch
 
-        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{self.local}")
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        dev = f"cuda:{self.device_index}" if self.backend == "nccl" else "cpu"
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op=op)
         return float(t.item())
+
+    def max(self, v: float) -> float:
+        return self._reduce(v, self.pg.ReduceOp.MAX) if self.pg else v
 
     def sum(self, v: float) -> float:
-        if not self.pg:
-            return v
-        import torch
-
-        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{self.local}")
-        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
-        return float(t.item())
+        return self._reduce(v, self.pg.ReduceOp.SUM) if self.pg else v
 
     def close(self):
         if self.pg:
@@ -284,7 +283,7 @@ def run_matern(args, D: Dist) -> dict:
     wl = WORKLOADS[args.workload]
     N = wl["N"]
     nus = wl["nus"]
-    dev = torch.device("cuda", D.local)
+    dev = torch.device("cuda", D.device_index)
     locs = make_locs(N)
     lxy = torch.from_numpy(np.ascontiguousarray(locs.T)).to(dev)
     lx, ly = lxy[0], lxy[1]
@@ -318,7 +317,7 @@ def run_matern(args, D: Dist) -> dict:
     torch.cuda.synchronize(dev)
     D.barrier()
     torch.cuda.synchronize(dev)
-    clocks = ClockSampler(D.local)
+    clocks = ClockSampler(D.device_index)
     if D.rank == 0:
         clocks.start()
     launches0 = _lib.launch_count()
@@ -389,7 +388,7 @@ def run_besselk(args, D: Dist) -> dict:
     from paper_2502_00356_b200.besselk import _launch_besselk
 
     n_total = WORKLOADS["bk"]["n"]
-    dev = torch.device("cuda", D.local)
+    dev = torch.device("cuda", D.device_index)
     from paper_2502_00356_b200.distributed import batch_shard
 
     i0, i1 = batch_shard(n_total, D.world, D.rank)
@@ -485,11 +484,11 @@ def main():
         print(json.dumps(reference_line(args, D.world, wl, matern)), flush=True)
         return
 
-    D.init("nccl")
+    D.init()
     import torch
 
     peaks = peaks_file()
-    fp64 = measure_fp64_peak(torch.device("cuda", D.local)) if D.rank == 0 else None
+    fp64 = measure_fp64_peak(torch.device("cuda", D.device_index)) if D.rank == 0 else None
 
     if matern:
         r = run_matern(args, D)
