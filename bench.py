@@ -291,6 +291,8 @@ def run_matern(args, D: Dist) -> dict:
     plans = [matern_plan(bg.MaternParams(1.0, 0.1, nu), cfg) for nu in nus]
     packed = args.workload == "m200"
     ts = 256
+    pm = None
+    mode = "rows"
     if packed:
         ntiles = bg.lower_tile_count(N, ts)
         l0, l1 = tile_shard(ntiles, D.world, D.rank)
@@ -298,17 +300,39 @@ def run_matern(args, D: Dist) -> dict:
         computed_local = float((l1 - l0) * ts * ts)  # diagonal tiles are stored complete
         stored_local = computed_local
     else:
-        r0, r1 = row_shard(N, D.world, D.rank)
-        out = torch.empty((r1 - r0, N), dtype=torch.float64, device=dev)
-        R = r1 - r0
-        computed_local = float(computed_entries(N, r0, r1))
-        stored_local = float(R * N)
+        if D.world > 1 and args.mode in ("auto", "peer"):
+            from paper_2502_00356_b200.distributed import MACRO, PeerMatrix
+
+            try:
+                pm = PeerMatrix(N, device=dev)
+                mode = "peer"
+            except Exception as ex:  # noqa: BLE001 -- fall back to no-communication rows
+                log(f"peer mapping unavailable ({ex}); using independent row blocks")
+                if args.mode == "peer":
+                    raise
+        if pm is not None:
+            r0, r1, out = pm.r0, pm.r1, pm.block
+            lt = np.arange(*pm.tiles, dtype=np.int64)
+            pp = ((np.sqrt(8.0 * lt + 1.0) - 1.0) // 2).astype(np.int64)
+            pp += ((pp + 1) * (pp + 2) // 2 <= lt)
+            pp -= (pp * (pp + 1) // 2 > lt)
+            qq = lt - pp * (pp + 1) // 2
+            mm = np.minimum(MACRO, N - MACRO * pp)
+            nn_ = np.minimum(MACRO, N - MACRO * qq)
+            computed_local = float(np.sum(mm * nn_))
+        else:
+            r0, r1 = row_shard(N, D.world, D.rank)
+            out = torch.empty((r1 - r0, N), dtype=torch.float64, device=dev)
+            computed_local = float(computed_entries(N, r0, r1))
+        stored_local = float((r1 - r0) * N)
     stream = torch.cuda.current_stream(dev)
 
     def step():
         for plan in plans:
             if packed:
                 _lower_launch(plan, lx, ly, N, ts, l0, l1, out)
+            elif pm is not None:
+                pm.compute(plan, lx, ly)
             else:
                 _cov_launch(plan, lx, ly, N, r0, r1, out, N, _lib.LAYOUT_ROW_MAJOR)
 
@@ -345,17 +369,46 @@ def run_matern(args, D: Dist) -> dict:
     res = {"ms_per_step": ms, "launches": int(D.sum(float(launches))), "clocks": clk,
            "computed_entries": computed, "stored_entries": stored, "kernel_ms": kern_ms,
            "computed_local": computed_local, "stored_local": stored_local, "N": N,
-           "nus": nus}
+           "nus": nus, "mode": mode}
     # sanity: symmetry of a probe block + diagonal == sigma^2 (cheap, outside timing)
     if not packed and r1 - r0 >= 64:
         blk = out[:64, r0:r0 + 64]
         res["check_symmetric_diag_block"] = bool(torch.equal(blk, blk.T)) and bool(
             (torch.diagonal(blk) == 1.0).all())
+    # ---- e2e with host buffers -------------------------------------------------------
+    if not args.no_e2e and pm is not None:
+        # fused peer path: H2D of the locations, the kernel, barrier, D2H of this rank's rows
+        host = bg.empty_host_matrix(r1 - r0, N)
+        host_t = torch.from_numpy(host)
+        ts_ = []
+        for k in range(1 + max(1, min(args.steps, args.e2e_steps))):
+            D.barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            lxy2 = torch.from_numpy(np.ascontiguousarray(locs.T)).to(dev)
+            for plan in plans:
+                pm.compute(plan, lxy2[0], lxy2[1])
+            torch.cuda.synchronize(dev)
+            D.barrier()
+            host_t.copy_(out)
+            dt = time.perf_counter() - t0
+            v = D.max(dt)
+            if k:
+                ts_.append(v)
+        res["e2e_s"] = statistics.median(ts_)
+        res["e2e_h2d"] = float(locs.nbytes) * D.world
+        res["e2e_d2h"] = stored * 8.0
+        res["e2e_how"] = ("fused peer kernel per rank (locations H2D each step), barrier, "
+                          "D2H of the rank's rows into pinned host memory; wall clock, max over ranks")
+        del host, host_t
+    if pm is not None:
+        D.barrier()
+        pm.close()
     del out
     torch.cuda.empty_cache()
 
     # ---- e2e through the public API with host buffers ---------------------------------
-    if not args.no_e2e and not packed:
+    if not args.no_e2e and not packed and pm is None:
         host = bg.empty_host_matrix(r1 - r0, N)
         theta = bg.MaternParams(1.0, 0.1, nus[0])
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -464,6 +517,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="m100")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", choices=["auto", "peer", "rows"], default="auto",
+                    help="N>1 full-matrix sharding: fused P2P mirror stores (peer) or "
+                         "independent row blocks (rows); auto = peer with fallback")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
@@ -542,8 +598,10 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
             "data": "synthetic: rng(20250201).random((N,2)) unit-square locations",
             "config": {"workload": f"{workload}: {wl['desc']}", "N": N, "nu": nus,
                        "sigma2": 1.0, "beta": 0.1, "bins": 40, "t_window": [0.0, 9.0],
-                       "parallelism": f"row-block shards x{world}, no collective" if workload != "m200"
-                       else f"packed lower-tile shards x{world}",
+                       "parallelism": (f"packed lower-tile shards x{world}" if workload == "m200" else
+                                       f"fused compute + NVLink P2P mirror stores x{world}: each "
+                                       "lower 64x64 tile computed once" if r.get("mode") == "peer"
+                                       else f"row-block shards x{world}, no collective"),
                        "l2": "output matrix (80 GB at N=100K) >> 126 MB L2; every step rewrites it"},
             "entries_per_s": r["stored_entries"] * len(nus) / t,
             "computed_entries_per_s": r["computed_entries"] * len(nus) / t,
@@ -571,9 +629,10 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
         if "e2e_s" in r:
             line["e2e"] = {"value": r["e2e_s"], "unit": "s", "h2d_bytes_per_step": r["e2e_h2d"],
                            "d2h_bytes_per_step": r["e2e_d2h"],
-                           "how": "paper_2502_00356_b200.generate_covariance(numpy locs, theta, "
-                                  "rows=shard, out=pinned host array): H2D of the locations, "
-                                  "device row blocks, D2H of every row (wall clock, max over ranks)"}
+                           "how": r.get("e2e_how",
+                                        "paper_2502_00356_b200.generate_covariance(numpy locs, theta, "
+                                        "rows=shard, out=pinned host array): H2D of the locations, "
+                                        "device row blocks, D2H of every row (wall clock, max over ranks)")}
         if world == 1 and not args.no_cpu_baseline:
             locs = make_locs(N)
             c = cpu_matern_sample(N, nus[0], locs, target_s=args.cpu_sample_s)

@@ -158,6 +158,38 @@ int bgk_matern_lower_tiles(const bgk_matern_plan *plan, const double *lx, const 
                            int64_t N, int64_t tile_size, int64_t tile_begin, int64_t tile_end,
                            double *out, void *stream);
 
+/* ---- multi-GPU: fused compute + NVLink peer stores ---------------------------------- */
+
+#define BGK_MACRO_TILE 64
+#define BGK_MAX_PEERS 32
+#define BGK_IPC_HANDLE_BYTES 64
+
+/* Full N x N matrix over G owners (one GPU each).  Lower 64x64 macro tiles
+ * l in [tile_begin, tile_end) of the WHOLE matrix (l = p(p+1)/2 + q, q <= p,
+ * T = ceil(N/64) macro rows) are each computed once: tile (p, q) is stored at its
+ * row owner and, for p != q, its transpose at its column owner.  Owner h holds
+ * macro rows [macro_row_start[h], macro_row_start[h+1]) -- matrix rows
+ * [64 start[h], min(N, 64 start[h+1])) -- row-major with ld = N at bases[h], a
+ * local pointer or a peer pointer mapped with bgk_ipc_open (NVLink P2P stores).
+ * macro_row_start[0] = 0, macro_row_start[G] = T, non-decreasing.  Equal ranges
+ * of [0, T(T+1)/2) over the ranks are equal work: every rank computes N^2/(2G)
+ * entries instead of the (1/G - 1/(2G^2)) N^2 of the no-communication row blocks.
+ * The matrix is complete once every rank's launch has finished (barrier). */
+int bgk_matern_covariance_peer(const bgk_matern_plan *plan, const double *lx, const double *ly,
+                               int64_t N, int G, const int64_t *macro_row_start,
+                               double *const *bases, int64_t tile_begin, int64_t tile_end,
+                               void *stream);
+
+/* CUDA IPC for one-process-per-GPU peer mapping.  export: handle (64 bytes) of the
+ * allocation holding ptr and ptr's offset in it.  open: map a peer's allocation on
+ * the current device and return base + offset.  close: unmap (pass the pointer
+ * open returned and the same offset). */
+int bgk_ipc_export(const void *ptr, void *handle, uint64_t *offset);
+int bgk_ipc_open(const void *handle, uint64_t offset, void **ptr);
+int bgk_ipc_close(void *ptr, uint64_t offset);
+/* cudaDeviceEnablePeerAccess(peer) on the current device; already-enabled is OK. */
+int bgk_enable_peer_access(int peer_device);
+
 /* ---- misc ------------------------------------------------------------------------- */
 const char *bgk_last_error(void);
 int bgk_abi_version(void);

@@ -23,6 +23,9 @@ PATH_SERIES, PATH_INTEGRAL = 0, 1
 LAYOUT_ROW_MAJOR, LAYOUT_COL_MAJOR = 0, 1
 MAX_NODES = 1024
 MAX_BUCKETS = 1024
+MACRO_TILE = 64
+MAX_PEERS = 32
+IPC_HANDLE_BYTES = 64
 
 
 class BackendUnavailable(RuntimeError):
@@ -103,6 +106,13 @@ SIGNATURES = {
     "bgk_abi_version": (_int, []),
     "bgk_launch_count": (_i64, []),
     "bgk_fp64_probe": (_int, [_vp, _i64, _int, _vp, ctypes.POINTER(ctypes.c_double)]),
+    "bgk_matern_covariance_peer": (_int, [ctypes.POINTER(BgkMaternPlan), _vp, _vp, _i64, _int,
+                                          ctypes.POINTER(ctypes.c_int64),
+                                          ctypes.POINTER(ctypes.c_void_p), _i64, _i64, _vp]),
+    "bgk_ipc_export": (_int, [_vp, _vp, ctypes.POINTER(ctypes.c_uint64)]),
+    "bgk_ipc_open": (_int, [_vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
+    "bgk_ipc_close": (_int, [_vp, ctypes.c_uint64]),
+    "bgk_enable_peer_access": (_int, [_int]),
 }
 
 _lock = threading.Lock()

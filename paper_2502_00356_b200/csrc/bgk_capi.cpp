@@ -389,4 +389,118 @@ int bgk_matern_lower_tiles(const bgk_matern_plan *plan, const double *lx, const 
   return bgk_launch_matern(plan, A, BGK_MODE_LOWER, (cudaStream_t)stream);
 }
 
+int bgk_matern_covariance_peer(const bgk_matern_plan *plan, const double *lx, const double *ly,
+                               int64_t N, int G, const int64_t *macro_row_start,
+                               double *const *bases, int64_t tile_begin, int64_t tile_end,
+                               void *stream) {
+  if (int rc = check_plan(plan)) return rc;
+  const int64_t T = (N + BGK_MACRO_TILE - 1) / BGK_MACRO_TILE;
+  const int64_t total = T * (T + 1) / 2;
+  if (N < 0 || G < 1 || G > BGK_MAX_PEERS || !macro_row_start || !bases || tile_begin < 0 ||
+      tile_end > total || tile_begin > tile_end) {
+    bgk_set_error("bgk_matern_covariance_peer: bad N/G/tile range");
+    return BGK_ERR_INVALID;
+  }
+  if (macro_row_start[0] != 0 || macro_row_start[G] != T) {
+    bgk_set_error("bgk_matern_covariance_peer: macro_row_start must run from 0 to ceil(N/64)");
+    return BGK_ERR_INVALID;
+  }
+  for (int h = 0; h < G; ++h) {
+    const bool empty = macro_row_start[h + 1] == macro_row_start[h];
+    if (macro_row_start[h + 1] < macro_row_start[h] || (!bases[h] && !empty)) {
+      bgk_set_error("bgk_matern_covariance_peer: bad owner %d", h);
+      return BGK_ERR_INVALID;
+    }
+  }
+  if (tile_end == tile_begin || N == 0) return BGK_OK;
+  if (!lx || !ly) {
+    bgk_set_error("bgk_matern_covariance_peer: NULL locations");
+    return BGK_ERR_INVALID;
+  }
+  BgkMaternArgs A{};
+  A.rx = lx; A.ry = ly; A.cx = lx; A.cy = ly; A.out = bases[0];
+  A.m = N; A.n = N; A.ld = N; A.layout = BGK_LAYOUT_ROW_MAJOR;
+  A.tile0 = tile_begin; A.tile1 = tile_end;
+  A.G = G;
+  for (int h = 0; h <= G; ++h) A.pstart[h] = macro_row_start[h];
+  for (int h = 0; h < G; ++h) A.bases[h] = bases[h];
+  return bgk_launch_matern(plan, A, BGK_MODE_PEER, (cudaStream_t)stream);
+}
+
+int bgk_ipc_export(const void *ptr, void *handle, uint64_t *offset) {
+  if (!ptr || !handle || !offset) {
+    bgk_set_error("bgk_ipc_export: NULL argument");
+    return BGK_ERR_INVALID;
+  }
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(ptr));
+  if (e != cudaSuccess) {
+    bgk_set_error("cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    return BGK_ERR_CUDA;
+  }
+  // offset of ptr inside its allocation (cuMemGetAddressRange via the runtime's
+  // driver entry point, so the library needs no -lcuda)
+  typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess || !fn) {
+      bgk_set_error("cuMemGetAddressRange unavailable");
+      return BGK_ERR_CUDA;
+    }
+    get_range = (GetRange)fn;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (unsigned long long)(uintptr_t)ptr) != 0) {
+    bgk_set_error("cuMemGetAddressRange failed");
+    return BGK_ERR_CUDA;
+  }
+  static_assert(sizeof(h) == BGK_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = (uint64_t)((uintptr_t)ptr - base);
+  return BGK_OK;
+}
+
+int bgk_ipc_open(const void *handle, uint64_t offset, void **ptr) {
+  if (!handle || !ptr) {
+    bgk_set_error("bgk_ipc_open: NULL argument");
+    return BGK_ERR_INVALID;
+  }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void *base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    bgk_set_error("cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    return BGK_ERR_CUDA;
+  }
+  *ptr = (char *)base + offset;
+  return BGK_OK;
+}
+
+int bgk_ipc_close(void *ptr, uint64_t offset) {
+  cudaError_t e = cudaIpcCloseMemHandle((char *)ptr - offset);
+  if (e != cudaSuccess) {
+    bgk_set_error("cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+    return BGK_ERR_CUDA;
+  }
+  return BGK_OK;
+}
+
+int bgk_enable_peer_access(int peer_device) {
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return BGK_OK;
+  }
+  if (e != cudaSuccess) {
+    bgk_set_error("cudaDeviceEnablePeerAccess(%d): %s", peer_device, cudaGetErrorString(e));
+    return BGK_ERR_CUDA;
+  }
+  return BGK_OK;
+}
+
 }  // extern "C"

@@ -20,7 +20,9 @@ int bgk_launch_log_integrand(const double *t, const double *x, const double *nu,
                              int order, double *out, cudaStream_t stream);
 
 // Matern launch descriptor (one of three task decoders)
-enum BgkMaternMode { BGK_MODE_TILE = 0, BGK_MODE_COV = 1, BGK_MODE_LOWER = 2 };
+enum BgkMaternMode { BGK_MODE_TILE = 0, BGK_MODE_COV = 1, BGK_MODE_LOWER = 2, BGK_MODE_PEER = 3 };
+
+#define BGK_MAX_PEERS 32
 
 struct BgkMaternArgs {
   const double *rx, *ry;  // row locations (COV/LOWER: all N locations)
@@ -37,6 +39,11 @@ struct BgkMaternArgs {
   long long nTr, nL, nR, nD;
   // LOWER decode helpers (filled by bgk_launch_matern)
   long long sub, subc;    // sub-tiles per storage tile: rows, cols
+  // PEER: G row-block owners; owner h holds macro rows [pstart[h], pstart[h+1])
+  // (rows [64 pstart[h], min(N, 64 pstart[h+1]))) at bases[h], row-major, ld = N.
+  int G;
+  long long pstart[BGK_MAX_PEERS + 1];
+  double *bases[BGK_MAX_PEERS];
 };
 
 int bgk_launch_matern(const bgk_matern_plan *plan, BgkMaternArgs &args, int mode,

@@ -135,3 +135,146 @@ def bessel_k_batch_sharded(x, nu, cfg=None, *, group=None, gather: bool = False,
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
     return 0, n, torch.cat([b[:e - s] for b, (s, e) in zip(bufs, sizes)])
+
+
+# ---------------------------------------------------------------------------------------
+# fused compute + NVLink peer stores (every lower macro tile computed exactly once)
+# ---------------------------------------------------------------------------------------
+
+MACRO = 64
+
+
+def macro_row_starts(N: int, world: int) -> list[int]:
+    """Owner h holds macro rows [s[h], s[h+1]) (64-row blocks), as equal as possible."""
+    T = -(-N // MACRO)
+    return [T * g // world for g in range(world + 1)]
+
+
+def owner_rows(N: int, world: int, rank: int) -> tuple[int, int]:
+    s = macro_row_starts(N, world)
+    return min(N, MACRO * s[rank]), min(N, MACRO * s[rank + 1])
+
+
+def peer_tile_range(N: int, world: int, rank: int) -> tuple[int, int]:
+    """This rank's equal share of the T(T+1)/2 lower macro tiles (equal work)."""
+    T = -(-N // MACRO)
+    total = T * (T + 1) // 2
+    return total * rank // world, total * (rank + 1) // world
+
+
+def _launch_peer(plan, lx, ly, N, starts, bases, l0, l1):
+    import ctypes
+
+    import torch
+
+    from . import _lib
+
+    L = _lib.lib()
+    G = len(bases)
+    st = (ctypes.c_int64 * (G + 1))(*starts)
+    bp = (ctypes.c_void_p * G)(*bases)
+    rc = L.bgk_matern_covariance_peer(ctypes.byref(plan), lx.data_ptr(), ly.data_ptr(), N, G, st,
+                                      bp, l0, l1, torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "bgk_matern_covariance_peer")
+
+
+def generate_covariance_peer_emulated(locs, theta, world: int, cfg=None):
+    """Single-process check of the peer-store kernel: ``world`` owner buffers on the
+    current GPU stand in for the ranks' HBM and every rank's tile range is
+    launched here.  Returns the owners' row blocks (their concatenation is the
+    full matrix)."""
+    import torch
+
+    from .besselk import DEFAULT_CONFIG
+    from .covariance import _coords, matern_plan
+
+    lx, ly = _coords(locs)
+    N = lx.numel()
+    plan = matern_plan(theta, cfg or DEFAULT_CONFIG)
+    starts = macro_row_starts(N, world)
+    blocks = []
+    for g in range(world):
+        r0, r1 = owner_rows(N, world, g)
+        blocks.append(torch.empty((r1 - r0, N), dtype=torch.float64, device=lx.device))
+    bases = [b.data_ptr() for b in blocks]
+    for g in range(world):
+        l0, l1 = peer_tile_range(N, world, g)
+        _launch_peer(plan, lx, ly, N, starts, bases, l0, l1)
+    return blocks
+
+
+class PeerMatrix:
+    """This rank's row block plus IPC mappings of every other rank's block.
+
+    Collective construction (all ranks of ``group``): allocate the local block,
+    export a CUDA IPC handle, all-gather the handles, enable peer access and map
+    the peers.  ``compute`` then runs this rank's tile range of the fused kernel;
+    the whole matrix is complete after ``compute`` on every rank plus a barrier.
+    """
+
+    def __init__(self, N: int, group=None, device=None):
+        import ctypes
+
+        import torch
+
+        from . import _lib
+
+        dist = _dist()
+        self.group = group
+        self.rank, self.world = _rank_world(group)
+        self.N = N
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.r0, self.r1 = owner_rows(N, self.world, self.rank)
+        self.block = torch.empty((self.r1 - self.r0, N), dtype=torch.float64, device=self.device)
+        L = _lib.lib()
+        handle = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
+        off = ctypes.c_uint64()
+        ptr = self.block.data_ptr() if self.block.numel() else 0
+        if ptr:
+            _lib.check(L.bgk_ipc_export(ptr, handle, ctypes.byref(off)), "bgk_ipc_export")
+        mine = (bytes(handle.raw), int(off.value), self.device.index, bool(ptr))
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.bases, self._opened = [], []
+        for h, (hb, o, dev, ok) in enumerate(everyone):
+            if h == self.rank or not ok:
+                self.bases.append(ptr or 1)  # empty blocks are never written
+                continue
+            if dev != self.device.index:
+                _lib.check(L.bgk_enable_peer_access(dev), "bgk_enable_peer_access")
+            p = ctypes.c_void_p()
+            _lib.check(L.bgk_ipc_open(hb, o, ctypes.byref(p)), "bgk_ipc_open")
+            self.bases.append(p.value)
+            self._opened.append((p.value, o))
+        self.starts = macro_row_starts(N, self.world)
+        self.tiles = peer_tile_range(N, self.world, self.rank)
+
+    def compute(self, plan, lx, ly):
+        """Launch this rank's tiles (stream-ordered; no barrier)."""
+        _launch_peer(plan, lx, ly, self.N, self.starts, self.bases, *self.tiles)
+
+    def close(self):
+        from . import _lib
+
+        L = _lib.load_library()
+        for p, o in self._opened:
+            L.bgk_ipc_close(p, o)
+        self._opened = []
+
+
+def generate_covariance_peer(locs, theta, cfg=None, *, group=None, device=None):
+    """Row block of this rank, with every lower macro tile of the matrix computed
+    once across the group and transposes stored straight into the owning GPU's
+    memory over NVLink.  Returns (r0, r1, block); collective."""
+    import torch
+
+    from .besselk import DEFAULT_CONFIG
+    from .covariance import _coords, matern_plan
+
+    lx, ly = _coords(locs)
+    pm = PeerMatrix(lx.numel(), group=group, device=device)
+    pm.compute(matern_plan(theta, cfg or DEFAULT_CONFIG), lx, ly)
+    torch.cuda.synchronize(pm.device)
+    _dist().barrier(group=group)
+    pm.close()
+    return pm.r0, pm.r1, pm.block

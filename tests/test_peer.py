@@ -1,0 +1,90 @@
+"""GPU tests of the fused compute + peer-store path (bgk_matern_covariance_peer):
+every lower macro tile computed once, stored at its row owner and mirrored into
+its column owner's memory.  One GPU: (1) in-process emulation with G owner
+buffers on the device; (2) two processes sharing the GPU through CUDA IPC, the
+exact code path of the one-process-per-GPU NVLink run."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("N,G", [(1000, 2), (1000, 3), (777, 8), (130, 5), (64, 4), (2113, 7)])
+def test_peer_emulated_union_is_full_matrix(N, G):
+    import paper_2502_00356_b200 as bg
+    from paper_2502_00356_b200 import distributed as D
+
+    rng = np.random.default_rng(N + G)
+    locs = rng.random((N, 2))
+    theta = bg.MaternParams(1.0, 0.1, 1.5)
+    full = bg.generate_covariance(locs, theta, device="cuda").data
+    blocks = D.generate_covariance_peer_emulated(locs, theta, G)
+    assert sum(b.shape[0] for b in blocks) == N
+    assert torch.equal(torch.cat(blocks, 0), full)
+
+
+def test_peer_work_is_balanced():
+    from paper_2502_00356_b200 import distributed as D
+
+    N, G = 100_000, 8
+    T = -(-N // 64)
+    sizes = [b - a for a, b in (D.peer_tile_range(N, G, g) for g in range(G))]
+    assert sum(sizes) == T * (T + 1) // 2 and max(sizes) - min(sizes) <= 1
+    # vs the no-communication row blocks: 8x instead of 4.27x over one GPU
+    nocomm = max(D.computed_entries(N, *D.row_shard(N, G, g)) for g in range(G))
+    assert nocomm / (N * (N + 1) / 2) > 0.23 and max(sizes) * 64 * 64 / (N * N / 2) < 0.126
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ipc_worker(rank, world, port, N, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    sys.path.insert(0, ROOT)
+    import paper_2502_00356_b200 as bg
+    from paper_2502_00356_b200 import distributed as D
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        locs = np.random.default_rng(7).random((N, 2))
+        theta = bg.MaternParams(1.3, 0.07, 0.8)
+        r0, r1, blk = D.generate_covariance_peer(locs, theta)
+        np.save(os.path.join(out_dir, f"blk{rank}.npy"), blk.cpu().numpy())
+        with open(os.path.join(out_dir, f"rows{rank}"), "w") as fh:
+            fh.write(f"{r0} {r1}")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_two_processes_cuda_ipc(tmp_path):
+    import paper_2502_00356_b200 as bg
+
+    N, world = 1500, 2
+    mp.start_processes(_ipc_worker, args=(world, _free_port(), N, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    locs = np.random.default_rng(7).random((N, 2))
+    full = bg.generate_covariance(locs, bg.MaternParams(1.3, 0.07, 0.8), device="cuda").to_numpy()
+    got = []
+    for r in range(world):
+        r0, r1 = map(int, open(os.path.join(tmp_path, f"rows{r}")).read().split())
+        blk = np.load(os.path.join(tmp_path, f"blk{r}.npy"))
+        assert blk.shape == (r1 - r0, N)
+        got.append(blk)
+    assert np.array_equal(np.concatenate(got, 0), full)
