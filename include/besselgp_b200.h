@@ -158,6 +158,19 @@ int bgk_matern_lower_tiles(const bgk_matern_plan *plan, const double *lx, const 
                            int64_t N, int64_t tile_size, int64_t tile_begin, int64_t tile_end,
                            double *out, void *stream);
 
+/* ---- location preprocessing --------------------------------------- */
+
+/* normalize_locations: out = clip((c - min) / max(extent_x, extent_y), 0, 1) per
+ * axis; `bounds` is 4 x uint64 of device scratch (order-mapped min x, min y,
+ * max x, max y).  Bitwise equal to the host definition. */
+int bgk_normalize_locations(const double *x, const double *y, int64_t n, unsigned long long *bounds,
+                            double *out_x, double *out_y, void *stream);
+
+/* Morton keys for morton_order: q = floor(c (2^bits - 1)) per axis, bits
+ * interleaved with x in the low bit.  Sort the keys stably for the permutation. */
+int bgk_morton_keys(const double *x, const double *y, int64_t n, int bits_per_axis,
+                    uint64_t *keys, void *stream);
+
 /* ---- multi-GPU: fused compute + NVLink peer stores ---------------------------------- */
 
 #define BGK_MACRO_TILE 64

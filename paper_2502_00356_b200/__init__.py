@@ -46,6 +46,7 @@ from .covariance import (
     normalize_locations,
 )
 from ._lib import BackendError, BackendUnavailable
+from . import distributed, gp
 
 __all__ = [
     # reference besselgp/__init__.py:19-33

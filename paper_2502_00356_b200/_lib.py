@@ -113,6 +113,8 @@ SIGNATURES = {
     "bgk_ipc_open": (_int, [_vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
     "bgk_ipc_close": (_int, [_vp, ctypes.c_uint64]),
     "bgk_enable_peer_access": (_int, [_int]),
+    "bgk_normalize_locations": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "bgk_morton_keys": (_int, [_vp, _vp, _i64, _int, _vp, _vp]),
 }
 
 _lock = threading.Lock()

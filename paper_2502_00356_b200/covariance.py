@@ -161,6 +161,19 @@ class CovarianceMatrix:
             # column-major == transpose of row-major; Sigma is symmetric bitwise
             np.ascontiguousarray(a.T).astype("<f8", copy=False).tofile(fh)
 
+    # ---- CSV: row-major, 17 significant digits ------------------------
+    def write_csv(self, path: str) -> None:
+        if self.layout != "full":
+            raise DomainError("CSV holds a full-layout matrix (or row block)")
+        np.savetxt(path, self.to_numpy(), fmt="%.17g", delimiter=",")
+
+    @staticmethod
+    def read_csv(path: str) -> "CovarianceMatrix":
+        a = np.atleast_2d(np.loadtxt(path, delimiter=",", dtype=np.float64))
+        if a.shape[0] != a.shape[1]:
+            raise DomainError("CSV matrix must be square")
+        return CovarianceMatrix(N=a.shape[0], data=a)
+
     @staticmethod
     def read_cvmx(path: str) -> "CovarianceMatrix":
         with open(path, "rb") as fh:
@@ -471,8 +484,64 @@ def generate_covariance(locs, theta: MaternParams, cfg: QuadratureConfig = DEFAU
 # location preprocessing
 # ---------------------------------------------------------------------------------------
 
-def normalize_locations(raw: LocationSet) -> LocationSet:
-    """Map into the unit square with one scale factor l = max(extent_x, extent_y)."""
+def _is_cuda(a) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(a, torch.Tensor) and a.is_cuda
+
+
+def normalize_locations_device(coords):
+    """normalize_locations on the GPU for an (N, 2) CUDA tensor (bitwise equal to
+    the host version); returns a new (N, 2) float64 CUDA tensor."""
+    torch = _torch()
+    L = _lib.lib()
+    c = coords.to(dtype=torch.float64)
+    x, y = c[:, 0].contiguous(), c[:, 1].contiguous()
+    n = x.numel()
+    if n == 0:
+        raise DomainError("location set must be non-empty")
+    bounds = torch.empty(4, dtype=torch.int64, device=x.device)
+    ox, oy = torch.empty_like(x), torch.empty_like(y)
+    with torch.cuda.device(x.device):
+        _lib.check(L.bgk_normalize_locations(x.data_ptr(), y.data_ptr(), n, bounds.data_ptr(),
+                                             ox.data_ptr(), oy.data_ptr(), _stream()),
+                   "bgk_normalize_locations")
+    b = bounds.cpu().numpy().view(np.uint64)  # order-mapped doubles -> doubles
+    neg = (b >> np.uint64(63)) == 0
+    raw_bits = np.where(neg, ~b, b & np.uint64(0x7FFFFFFFFFFFFFFF))
+    mnx, mny, mxx, mxy = raw_bits.view(np.float64)
+    if max(mxx - mnx, mxy - mny) == 0.0:
+        raise DomainError("degenerate location set: all points coincide")
+    return torch.stack([ox, oy], 1)
+
+
+def morton_order_device(coords, bits_per_axis: int = 16):
+    """(reordered coords, permutation) on the GPU for normalized (N, 2) CUDA coords:
+    device Morton keys + a stable sort (ties keep the original order)."""
+    torch = _torch()
+    L = _lib.lib()
+    if not 1 <= bits_per_axis <= 31:
+        raise DomainError("bits_per_axis must lie in [1, 31]")
+    c = coords.to(dtype=torch.float64)
+    x, y = c[:, 0].contiguous(), c[:, 1].contiguous()
+    keys = torch.empty(x.numel(), dtype=torch.int64, device=x.device)
+    with torch.cuda.device(x.device):
+        _lib.check(L.bgk_morton_keys(x.data_ptr(), y.data_ptr(), x.numel(), bits_per_axis,
+                                     keys.data_ptr(), _stream()), "bgk_morton_keys")
+    # keys use at most 62 bits, so signed int64 order == unsigned order
+    perm = torch.sort(keys, stable=True).indices
+    return c[perm], perm
+
+
+def normalize_locations(raw):
+    """Map into the unit square with one scale factor l = max(extent_x, extent_y).
+
+    A LocationSet is normalized on the host; an (N, 2) CUDA tensor on the device
+    (``normalize_locations_device``, bitwise equal)."""
+    if _is_cuda(raw):
+        return normalize_locations_device(raw)
     c = raw.coords
     if c.shape[0] == 0:
         raise DomainError("location set must be non-empty")
@@ -496,10 +565,13 @@ def _part1by1(v: np.ndarray) -> np.ndarray:
     return v
 
 
-def morton_order(s: LocationSet, bits_per_axis: int = 16) -> tuple[LocationSet, np.ndarray]:
+def morton_order(s, bits_per_axis: int = 16):
     """Z-order permutation: quantise to floor(c (2^bits - 1)), interleave with x in
     the low bit, stable sort (ties keep the original order).  Returns the
-    reordered set and the permutation ``perm`` with new[i] = old[perm[i]]."""
+    reordered set and the permutation ``perm`` with new[i] = old[perm[i]].
+    An (N, 2) CUDA tensor of normalized coordinates is ordered on the device."""
+    if _is_cuda(s):
+        return morton_order_device(s, bits_per_axis)
     if not s.normalized:
         raise DomainError("morton_order needs a normalized LocationSet")
     if not 1 <= bits_per_axis <= 31:

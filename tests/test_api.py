@@ -171,3 +171,14 @@ def test_morton_permutation_equivariance_host():
     s = bg.normalize_locations(bg.LocationSet(rng.random((257, 2)) * 7.0))
     m, perm = bg.morton_order(s, bits_per_axis=10)
     assert np.array_equal(np.sort(perm), np.arange(257))
+
+
+def test_csv_roundtrip(tmp_path):
+    rng = np.random.default_rng(2)
+    a = rng.random((6, 6))
+    a = a + a.T
+    m = bg.CovarianceMatrix(N=6, data=a)
+    path = os.path.join(tmp_path, "m.csv")
+    m.write_csv(path)
+    assert open(path).readline().count(",") == 5
+    assert np.array_equal(bg.CovarianceMatrix.read_csv(path).data, a)
