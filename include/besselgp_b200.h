@@ -158,6 +158,22 @@ int bgk_matern_lower_tiles(const bgk_matern_plan *plan, const double *lx, const 
                            int64_t N, int64_t tile_size, int64_t tile_begin, int64_t tile_end,
                            double *out, void *stream);
 
+/* ---- accuracy audit (oracle.py, kernels.py:306-335) ------------------- */
+
+#define BGK_AUDIT_REFINED 0       /* refined_log10_grid (kernels.py:306-318)       */
+#define BGK_AUDIT_PURE_INTEGRAL 1 /* pure_integral_log10_grid (kernels.py:321-329) */
+#define BGK_AUDIT_ORACLE 2        /* dynamic-window oracle (oracle.py:92-160)      */
+
+/* log K over the nnu x nx (nu, x) grid (row-major out[i*nx + j]), one CTA per
+ * point, reference-faithful arithmetic: window search by FINDRANGE / FINDZERO
+ * (Newton + bisection, tol 1e-12) for the oracle with `bins` intervals
+ * (cfg->bins for the other methods), the series below cfg->small_x_threshold
+ * (not for PURE_INTEGRAL).  base10: 1 -> double-double base-10 assembly
+ * (kernels.py:97-109), 0 -> natural log.  Failed window searches give NaN. */
+int bgk_log_grid(const double *nus, int64_t nnu, const double *xs, int64_t nx,
+                 const bgk_config *cfg, int method, int64_t bins, int base10, double *out,
+                 void *stream);
+
 /* ---- location preprocessing --------------------------------------- */
 
 /* normalize_locations: out = clip((c - min) / max(extent_x, extent_y), 0, 1) per

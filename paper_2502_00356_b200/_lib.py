@@ -115,6 +115,8 @@ SIGNATURES = {
     "bgk_enable_peer_access": (_int, [_int]),
     "bgk_normalize_locations": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "bgk_morton_keys": (_int, [_vp, _vp, _i64, _int, _vp, _vp]),
+    "bgk_log_grid": (_int, [_vp, _i64, _vp, _i64, ctypes.POINTER(BgkConfig), _int, _i64, _int, _vp,
+                            _vp]),
 }
 
 _lock = threading.Lock()
