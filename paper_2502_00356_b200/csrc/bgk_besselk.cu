@@ -15,16 +15,22 @@
 //       2 cosh(a t_k) e^{-x c_k} / (e^{a t_a} e^{-x c_a}) = (E^{+-j} + q E^{-+j}) e^{-x (c_k - c_a)}
 //   so every node costs one table exp (7 FP64 ops) plus a handful of FP64 ops --
 //   no per-node log_cosh (the reference's 73% hot spot).
-//   c_k = cosh(t_k) is a per-CTA shared-memory table.  Both directions are
-//   walked in one loop (two independent exp chains) until the term falls below
-//   e^-50 of the anchor, which includes every node the reference's e^-46
-//   break keeps.       ln K = a t_a - ln2 - x c_a + ln(h acc)
+//   c_k = cosh(t_k) is a per-CTA shared-memory table.
+//       ln K = a t_a - ln2 - x c_a + ln(h acc)
 //
-// Divergence: walk lengths vary 1..40 over random (x, nu).  Each CTA stages its
-// 1024 elements in shared memory and counting-sorts them by a predicted walk
-// length (a host-built table over (log x, nu) cells), so a warp's 32 lanes walk
-// about the same number of nodes; Temme elements (x < thr) form their own
-// bucket.  Results go back through shared memory for coalesced stores.
+// Node window: a host-built table over (log x, nu) cells gives, relative to the
+// anchor, how far up and down the terms stay above e^-40 of the anchor term
+// (maximised over a 5 x 5 sample of the cell, plus a 1-node margin); each lane
+// sums its window [m - D, m + U] as one ascending sequence.  The reference's
+// walk also keeps terms in (e^-46, e^-40]: each is < 4e-18 of the sum, so
+// dropping them is below an ulp.  Elements outside the table's range use the
+// full grid [0, bins].
+//
+// Divergence: window sizes vary 1..40 over random (x, nu).  Each CTA stages its
+// 1024 elements in shared memory and counting-sorts them by predicted window
+// size, so a warp's 32 lanes sum about the same number of nodes; Temme elements
+// (x < thr) form their own bucket.  Results go back through shared memory for
+// coalesced stores.
 // Every value is a pure function of (x, nu, cfg): bitwise independent of batch
 // composition.
 #include <cuda_runtime.h>
@@ -46,7 +52,7 @@ constexpr int kBkChunk = kBkThreads * kBkPerThread;
 constexpr int kXCells = 64;   // x cells: 4 per octave from 2^-6
 constexpr int kNuCells = 48;  // nu cells: width 1/2, last one open-ended
 constexpr int kXKeyBase = (1023 - 6) << 2;
-constexpr int kMaxPred = 63;  // predicted walk steps, clamped
+constexpr int kMaxPred = 63;  // predicted window size (sort key), clamped
 constexpr int kBuckets = kMaxPred + 2;  // + series bucket
 
 struct BkArgs {
@@ -61,7 +67,7 @@ struct BkArgs {
   int bins;
   int route;
   int table_ok;  // 1: c table fits in shared memory and t0 >= 0 -> fast path allowed
-  const uint8_t *pred;  // device: predicted max(up, down) walk steps per (x, nu) cell
+  const uint32_t *win;  // device: per (x, nu) cell, U | D << 16 (window above / below anchor)
 };
 
 __host__ __device__ inline int x_cell(double x) {
@@ -88,59 +94,54 @@ __host__ __device__ inline int anchor_node(double x, double a, double t0, double
   return (int)fm;
 }
 
+__device__ __forceinline__ bool in_table(double x, double a) {
+  const int key = (int)((uint64_t)__double_as_longlong(x) >> 50) - kXKeyBase;
+  return key >= 0 && key < kXCells && a * 2.0 < (double)(kNuCells - 1);
+}
+
 // Fast fixed-window quadrature (see file header).  Requires t0 >= 0 and
-// a * max(|t0|, |t1|) <= 600 so that E^j never overflows.
-__device__ __forceinline__ double fixed_window_fast(double x, double a, const BkArgs &A,
-                                                    const double *__restrict__ ctab,
+// a * max(|t0|, |t1|) <= 600 so that E^{+-j} never overflows.  Called by ALL 32
+// lanes of a warp (inactive lanes sum nothing): lane i sums nodes lo_i .. hi_i
+// in ascending order, one node per loop trip, masked once its window is done.
+// Each node: s_k = E^{k-m} + q E^{m-k} carried by two running products,
+// term = s_k e^{x (c_m - c_k)} (table exp).  The value depends only on the
+// lane's own (x, nu).
+__device__ __forceinline__ double fixed_window_fast(bool active, double x, double a, uint32_t w,
+                                                    const BkArgs &A,
+                                                    const double2 *__restrict__ cw,
                                                     const double *__restrict__ t128,
                                                     const double *__restrict__ invc,
                                                     const double *__restrict__ logc) {
   const int bins = A.bins;
-  const int m = anchor_node(x, a, A.t0, A.h, bins);
+  const int m = active ? anchor_node(x, a, A.t0, A.h, bins) : 0;
+  const int U = min((int)(w & 0xffff), bins - m), D = min((int)(w >> 16), m);
+  const int lo = m - D, n = active ? U + D + 1 : 0;
   const double ta = A.t0 + (double)m * A.h;
-  const double ca = ctab[m];
+  const double ca = cw[m].x;
+  const double tlo = A.t0 + (double)lo * A.h;
   const double E = exp_acc(a * A.h, t128);
   const double Ei = exp_acc(-a * A.h, t128);
-  const double two_at = 2.0 * a * ta;
-  const double q = (two_at < 700.0) ? exp_acc(-two_at, t128) : 0.0;
-  const double anchor = 1.0 + q;
-  const double tiny = 1.9287498479639178e-22 * anchor;  // e^-50 of the anchor term
+  double P = exp_acc(-a * (ta - tlo), t128);  // E^{lo - m}
+  const double qa = a * (ta + tlo);
+  double Qs = (qa < 700.0) ? exp_acc(-qa, t128) : 0.0;  // q E^{m - lo}
   const double mx = -x, xca = x * ca;
-  double acc = ((m == 0 || m == bins) ? 0.5 : 1.0) * anchor;
-
-  double pu = 1.0, qu = 1.0, pd = 1.0, qd = 1.0;
-  bool up = m < bins, dn = m > 0;
-  int j = 1;
-  while (up || dn) {
-    if (up) {
-      pu *= E;
-      qu *= Ei;
-      const int k = m + j;
-      const double s = fma(q, qu, pu);
-      const double y = fmax(fma(mx, ctab[k], xca), -700.0);
-      const double term = s * exp_node(y, t128);
-      if (term < tiny) {
-        up = false;
-      } else {
-        acc = fma((k == bins) ? 0.5 : 1.0, term, acc);
-        up = k < bins;
-      }
-    }
-    if (dn) {
-      pd *= Ei;
-      qd *= E;
-      const int k = m - j;
-      const double s = fma(q, qd, pd);
-      const double y = fmax(fma(mx, ctab[k], xca), -700.0);
-      const double term = s * exp_node(y, t128);
-      if (term < tiny) {
-        dn = false;
-      } else {
-        acc = fma((k == 0) ? 0.5 : 1.0, term, acc);
-        dn = k > 0;
-      }
-    }
-    ++j;
+  double acc = 0.0;
+  // two nodes per trip (one warp vote per pair); same per-lane order as one by one.
+  // cw[k] = {c_k, ln w_k}: the trapezoid weight rides in the exponent.
+  for (int j = 0; __any_sync(0xffffffffu, j < n); j += 2) {
+    const double2 c0 = cw[min(lo + j, bins)], c1 = cw[min(lo + j + 1, bins)];
+    const double y0 = fmax(fma(mx, c0.x, xca), -700.0) + c0.y;
+    const double y1 = fmax(fma(mx, c1.x, xca), -700.0) + c1.y;
+    const double s0 = P + Qs;
+    P *= E;
+    Qs *= Ei;
+    const double s1 = P + Qs;
+    P *= E;
+    Qs *= Ei;
+    const double t0 = s0 * exp_node(y0, t128);
+    const double t1 = s1 * exp_node(y1, t128);
+    acc = (j < n) ? acc + t0 : acc;
+    acc = (j + 1 < n) ? acc + t1 : acc;
   }
   return (a * ta - kLn2) - xca + log_fast(A.h * acc, invc, logc);
 }
@@ -152,20 +153,15 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
   __shared__ uint16_t perm[kBkChunk];
   __shared__ uint8_t spath[kBkChunk];
   __shared__ int hist[kBuckets + 1];
-  __shared__ uint8_t spred[kXCells * kNuCells];
   __shared__ int s_next;
-  double *ctab = smem;  // bins + 1 (only when table_ok)
+  double2 *cw = reinterpret_cast<double2 *>(smem);  // {cosh t_k, ln w_k}, bins + 1
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   load_tables128(s_exp, s_invc, s_logc);
   if (A.table_ok)
-    for (int k = tid; k <= A.bins; k += kBkThreads) ctab[k] = cosh(A.t0 + (double)k * A.h);
+    for (int k = tid; k <= A.bins; k += kBkThreads)
+      cw[k] = make_double2(cosh(A.t0 + (double)k * A.h), (k == 0 || k == A.bins) ? -kLn2 : 0.0);
   for (int b = tid; b <= kBuckets; b += kBkThreads) hist[b] = 0;
-  if (A.table_ok) {
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(A.pred);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(spred);
-    for (int c = tid; c < kXCells * kNuCells / 4; c += kBkThreads) dst[c] = __ldg(src + c);
-  }
   if (tid == 0) s_next = 0;
 
   const long long base = (long long)blockIdx.x * kBkChunk;
@@ -178,13 +174,20 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
   __syncthreads();
 
   const double tmax = fmax(fabs(A.t0), fabs(A.t1));
+  // window word of an element: the table cell, or the full grid outside its range
+  auto window_of = [&](double x, double a) -> uint32_t {
+    if (in_table(x, a)) return __ldg(A.win + x_cell(x) * kNuCells + nu_cell(a));
+    return (uint32_t)A.bins | ((uint32_t)A.bins << 16);
+  };
   auto bucket_of = [&](double x, double nu) -> int {
     const bool series = (A.route == 1) || (A.route == 0 && x < A.thr);
     if (series) return 0;
     const double a = fabs(nu);
     if (!(A.table_ok && a * tmax <= 600.0)) return kBuckets - 1;  // general path: last
-    // longest predicted walks first (they are pulled first in the compute phase)
-    return kMaxPred - min((int)spred[x_cell(x) * kNuCells + nu_cell(a)], kMaxPred - 1);
+    // widest predicted windows first (they are pulled first in the compute phase)
+    const uint32_t w = window_of(x, a);
+    const int n = (int)(w & 0xffff) + (int)(w >> 16) + 1;
+    return kMaxPred - min(n, kMaxPred - 1);
   };
   for (int e = tid; e < cnt; e += kBkThreads) atomicAdd(&hist[bucket_of(sx[e], snu[e])], 1);
   __syncthreads();
@@ -213,27 +216,28 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
   __syncthreads();
 
   // compute in sorted order: warps pull 32-element groups from a shared counter,
-  // longest predicted walks first
+  // widest predicted windows first.  Every lane of the warp enters the fast sum
+  // (lanes without a fast-path element sum nothing) so it runs branch-free.
   const int ngroups = (cnt + 31) >> 5;
   for (;;) {
     int g = lane == 0 ? atomicAdd(&s_next, 1) : 0;
     g = __shfl_sync(0xffffffffu, g, 0);
     if (g >= ngroups) break;
     const int p = g * 32 + lane;
-    if (p >= cnt) continue;
-    const int e = perm[p];
-    const double x = sx[e], nu = snu[e];
+    const bool valid = p < cnt;
+    const int e = valid ? perm[p] : 0;
+    const double x = valid ? sx[e] : 1.0, nu = valid ? snu[e] : 0.0;
     const bool series = (A.route == 1) || (A.route == 0 && x < A.thr);
-    double lk;
+    const double a = fabs(nu);
+    const bool fast = valid && !series && A.table_ok && a * tmax <= 600.0;
+    const uint32_t w = fast ? window_of(x, a) : 0u;
+    double lk = fixed_window_fast(fast, x, a, w, A, cw, s_exp, s_invc, s_logc);
+    if (!valid) continue;
     if (series) {
       const TemmeConst T = temme_const(nu);
       lk = temme_series_log_c(x, T, A.eps, A.cap);
-    } else {
-      const double a = fabs(nu);
-      if (A.table_ok && a * tmax <= 600.0)
-        lk = fixed_window_fast(x, a, A, ctab, s_exp, s_invc, s_logc);
-      else
-        lk = fixed_window_log_ref(x, nu, A.t0, A.t1, A.bins);
+    } else if (!fast) {
+      lk = fixed_window_log_ref(x, nu, A.t0, A.t1, A.bins);
     }
     sx[e] = lk;
     if (A.k) snu[e] = (fabs(lk) < 700.0) ? exp_acc(lk, s_exp) : exp(lk);
@@ -290,53 +294,61 @@ __global__ void log_integrand_kernel(const double *t, const double *x, const dou
 // host: the walk-length prediction table, cached per (t0, t1, bins)
 // ---------------------------------------------------------------------------------
 
-// Host emulation of fixed_window_fast's walk length max(up, down) (libm exp).
-static int walk_steps_host(double x, double a, double t0, double h, int bins, const double *c) {
+// Host emulation of the reference-style walk from the fast path's anchor: how
+// many nodes above (up) and below (down) the anchor have a term >= e^-40 of it.
+// (The reference keeps terms down to e^-46 of its grid max; the ones in between
+// are < 4e-18 of the sum each, far below an ulp.)
+static void walk_extent_host(double x, double a, double t0, double h, int bins, const double *c,
+                             int &up, int &dn) {
   const int m = anchor_node(x, a, t0, h, bins);
   const double ta = t0 + m * h, ca = c[m];
   const double E = std::exp(a * h), Ei = std::exp(-a * h);
   const double q = (2 * a * ta < 700) ? std::exp(-2 * a * ta) : 0.0;
-  const double tiny = 1.9287498479639178e-22 * (1 + q);
-  int up = 0, dn = 0;
+  const double tiny = 4.248354255291589e-18 * (1 + q);  // e^-40
+  up = dn = 0;
   double p = 1, qq = 1;
   for (int j = 1; m + j <= bins; ++j) {
     p *= E;
     qq *= Ei;
-    ++up;
     if ((q * qq + p) * std::exp(std::fmax(-x * (c[m + j] - ca), -700.0)) < tiny) break;
+    up = j;
   }
   p = 1;
   qq = 1;
   for (int j = 1; m - j >= 0; ++j) {
     p *= Ei;
     qq *= E;
-    ++dn;
     if ((q * qq + p) * std::exp(std::fmax(-x * (c[m - j] - ca), -700.0)) < tiny) break;
+    dn = j;
   }
-  return up > dn ? up : dn;
 }
 
-static void build_pred_table(double t0, double t1, int bins, uint8_t *pred) {
+// Per (x, nu) cell: U | D << 16, the largest up / down extents over a 5 x 5 sample
+// of the cell, plus a 1-node margin.
+static void build_window_table(double t0, double t1, int bins, uint32_t *win) {
   std::vector<double> c(bins + 1);
   const double h = (t1 - t0) / bins;
   for (int k = 0; k <= bins; ++k) c[k] = std::cosh(t0 + k * h);
   for (int xi = 0; xi < kXCells; ++xi) {
-    // cell xi covers [2^(e) * (1 + f/4), 2^e * (1 + (f+1)/4)) with e, f from the key
     const int key = xi + kXKeyBase;
     const double lo = std::ldexp(1.0 + (key & 3) / 4.0, (key >> 2) - 1023);
     const double hi = std::ldexp(1.0 + ((key & 3) + 1) / 4.0, (key >> 2) - 1023);
     for (int ni = 0; ni < kNuCells; ++ni) {
       const double nlo = ni * 0.5;
-      const double nhi = (ni == kNuCells - 1) ? nlo + 8.0 : nlo + 0.5;
-      int best = 0;
-      for (int sx = 0; sx <= 2; ++sx)
-        for (int sn = 0; sn <= 2; ++sn) {
-          const double xv = lo + (hi - lo) * sx / 2.0 * 0.999;
-          const double nv = nlo + (nhi - nlo) * sn / 2.0 * 0.999;
-          const int w = walk_steps_host(xv, nv, t0, h, bins, c.data());
-          best = w > best ? w : best;
+      const double nhi = nlo + 0.5;
+      int U = 0, D = 0;
+      for (int sx = 0; sx <= 4; ++sx)
+        for (int sn = 0; sn <= 4; ++sn) {
+          const double xv = lo + (hi - lo) * sx / 4.0 * 0.9999;
+          const double nv = nlo + (nhi - nlo) * sn / 4.0 * 0.9999;
+          int up, dn;
+          walk_extent_host(xv, nv, t0, h, bins, c.data(), up, dn);
+          U = std::max(U, up);
+          D = std::max(D, dn);
         }
-      pred[xi * kNuCells + ni] = (uint8_t)(best > kMaxPred ? kMaxPred : best);
+      U = std::min(U + 1, bins);
+      D = std::min(D + 1, bins);
+      win[xi * kNuCells + ni] = (uint32_t)U | ((uint32_t)D << 16);
     }
   }
 }
@@ -346,12 +358,12 @@ static void build_pred_table(double t0, double t1, int bins, uint8_t *pred) {
 // ---------------------------------------------------------------------------------
 // launchers (called from bgk_capi.cpp)
 // ---------------------------------------------------------------------------------
-// Device copies of the walk-length prediction table, one per (t0, t1, bins), built
-// on the host and uploaded once (3 KB each); kept for the life of the process.
+// Device copies of the node-window table, one per (t0, t1, bins), built on the
+// host and uploaded once (12 KB each); kept for the life of the process.
 struct PredEntry {
   double t0, t1;
   long long bins;
-  uint8_t *dev;
+  uint32_t *dev;
 };
 
 int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
@@ -374,32 +386,33 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
   A.cap = cfg->series_cap;
   A.bins = (int)cfg->bins;
   A.route = route;
-  const int64_t kMaxTable = 16383;  // 128 KB of shared memory
+  const int64_t kMaxTable = 8191;  // 128 KB of shared memory ({c, ln w} pairs)
   A.table_ok = (cfg->t_lower >= 0.0 && cfg->bins <= kMaxTable) ? 1 : 0;
-  A.pred = nullptr;
+  A.win = nullptr;
   if (A.table_ok) {
     std::lock_guard<std::mutex> lock(mu);
     for (const PredEntry &e : cache)
-      if (e.t0 == cfg->t_lower && e.t1 == cfg->t_upper && e.bins == cfg->bins) A.pred = e.dev;
-    if (!A.pred) {
-      std::vector<uint8_t> host(bgk::kXCells * bgk::kNuCells);
-      bgk::build_pred_table(cfg->t_lower, cfg->t_upper, (int)cfg->bins, host.data());
-      uint8_t *dev = nullptr;
-      cudaError_t err = cudaMalloc(&dev, host.size());
-      if (err == cudaSuccess) err = cudaMemcpy(dev, host.data(), host.size(), cudaMemcpyHostToDevice);
+      if (e.t0 == cfg->t_lower && e.t1 == cfg->t_upper && e.bins == cfg->bins) A.win = e.dev;
+    if (!A.win) {
+      std::vector<uint32_t> host(bgk::kXCells * bgk::kNuCells);
+      bgk::build_window_table(cfg->t_lower, cfg->t_upper, (int)cfg->bins, host.data());
+      uint32_t *dev = nullptr;
+      const size_t bytes = host.size() * sizeof(uint32_t);
+      cudaError_t err = cudaMalloc(&dev, bytes);
+      if (err == cudaSuccess) err = cudaMemcpy(dev, host.data(), bytes, cudaMemcpyHostToDevice);
       if (err != cudaSuccess) {
         bgk_set_error("besselk prediction table upload: %s", cudaGetErrorString(err));
         return BGK_ERR_CUDA;
       }
       cache.push_back({cfg->t_lower, cfg->t_upper, cfg->bins, dev});
-      A.pred = dev;
+      A.win = dev;
     }
   }
-  size_t smem = sizeof(double) * (A.table_ok ? (size_t)cfg->bins + 1 : 0);
+  size_t smem = sizeof(double2) * (A.table_ok ? (size_t)cfg->bins + 1 : 0);
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(bgk::besselk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * (kMaxTable + 1)));
+                         (int)(sizeof(double2) * (kMaxTable + 1)));
     attr_set = true;
   }
   long long grid = (n + bgk::kBkChunk - 1) / bgk::kBkChunk;
