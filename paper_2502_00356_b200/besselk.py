@@ -180,6 +180,11 @@ def bessel_k_batch(x, nu, cfg: QuadratureConfig = DEFAULT_CONFIG, route: str = "
     if route not in _ROUTES:
         raise DomainError(f"route must be one of {sorted(_ROUTES)}")
     on_device = isinstance(x, torch.Tensor) and x.is_cuda
+    if not on_device and not isinstance(nu, torch.Tensor):
+        xa = np.asarray(x, dtype=np.float64)
+        na = np.asarray(nu, dtype=np.float64)
+        if xa.shape == na.shape and xa.size >= _HOST_CHUNK:
+            return _bessel_k_host_pipelined(xa, na, cfg, route, validate)
     xd = _to_device(x)
     nud = _to_device(nu, xd.device)
     if xd.shape != nud.shape:
@@ -188,23 +193,79 @@ def bessel_k_batch(x, nu, cfg: QuadratureConfig = DEFAULT_CONFIG, route: str = "
     shape = xd.shape
     xd, nud = xd.reshape(-1), nud.reshape(-1)
     if validate and xd.numel():
-        bad_x = ~torch.isfinite(xd) | (xd <= 0.0)
-        bad_nu = ~torch.isfinite(nud) | (nud < 0.0)
-        if route == "series":
-            bad_x |= xd >= cfg.small_x_threshold
-        if bool(bad_x.any()) or bool(bad_nu.any()):
-            i = int(torch.nonzero(bad_x | bad_nu)[0])
-            xv, nv = float(xd[i]), float(nud[i])
-            EvalPoint(xv, nv)  # raises the reference's message for non-finite / negative
-            if route == "series":
-                raise DomainError(
-                    f"series path needs 0 < x < {cfg.small_x_threshold:g}, got {xv!r}")
-            raise DomainError("x must be positive (r = 0 is handled by the Matern kernel)")
+        _validate_batch(xd, nud, cfg, route)
     logk, k, path = _launch_besselk(xd, nud, cfg, _ROUTES[route])
     logk, k, path = logk.reshape(shape), k.reshape(shape), path.reshape(shape)
     if on_device:
         return BatchResult(logk, k, path)
     return BatchResult(logk.cpu().numpy(), k.cpu().numpy(), path.cpu().numpy())
+
+
+def _validate_batch(xd, nud, cfg, route):
+    torch = _torch()
+    bad_x = ~torch.isfinite(xd) | (xd <= 0.0)
+    bad_nu = ~torch.isfinite(nud) | (nud < 0.0)
+    if route == "series":
+        bad_x |= xd >= cfg.small_x_threshold
+    if bool(bad_x.any()) or bool(bad_nu.any()):
+        i = int(torch.nonzero(bad_x | bad_nu)[0])
+        xv, nv = float(xd[i]), float(nud[i])
+        EvalPoint(xv, nv)  # raises the reference's message for non-finite / negative
+        if route == "series":
+            raise DomainError(f"series path needs 0 < x < {cfg.small_x_threshold:g}, got {xv!r}")
+        raise DomainError("x must be positive (r = 0 is handled by the Matern kernel)")
+
+
+_HOST_CHUNK = 1 << 22  # elements per pipelined chunk for host (numpy) batches
+
+
+def _bessel_k_host_pipelined(xa, na, cfg, route, validate):
+    """Host arrays in / host arrays out, chunked so that the H2D copy of chunk i+1,
+    the kernel on chunk i and the D2H of chunk i-1 overlap (two streams); results
+    land directly in page-locked output arrays."""
+    torch = _torch()
+    _lib.lib()
+    shape = xa.shape
+    xf = np.ascontiguousarray(xa).reshape(-1)
+    nf = np.ascontiguousarray(na).reshape(-1)
+    n = xf.size
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out_l = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    out_k = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    out_p = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    nbuf = 2
+    bufs = [None] * nbuf
+    freed = [None] * nbuf
+    for ci, c0 in enumerate(range(0, n, _HOST_CHUNK)):
+        c1 = min(n, c0 + _HOST_CHUNK)
+        s = ci % nbuf
+        if freed[s] is not None:
+            comp.wait_event(freed[s])
+        xd = torch.from_numpy(xf[c0:c1]).to(dev, non_blocking=True)
+        nd = torch.from_numpy(nf[c0:c1]).to(dev, non_blocking=True)
+        if validate:
+            _validate_batch(xd, nd, cfg, route)
+        logk, k, path = _launch_besselk(xd, nd, cfg, _ROUTES[route])
+        done = torch.cuda.Event()
+        done.record(comp)
+        copy.wait_event(done)
+        with torch.cuda.stream(copy):
+            out_l[c0:c1].copy_(logk, non_blocking=True)
+            out_k[c0:c1].copy_(k, non_blocking=True)
+            out_p[c0:c1].copy_(path, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        # keep the chunk's device buffers alive until its D2H has been issued/done
+        logk.record_stream(copy)
+        k.record_stream(copy)
+        path.record_stream(copy)
+        bufs[s] = (logk, k, path)
+        freed[s] = ev
+    copy.synchronize()
+    return BatchResult(out_l.numpy().reshape(shape), out_k.numpy().reshape(shape),
+                       out_p.numpy().reshape(shape))
 
 
 def _scalar_logk(x: float, nu: float, cfg: QuadratureConfig, route: int,

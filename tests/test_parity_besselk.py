@@ -181,3 +181,26 @@ def test_log_integrand_family(bg, golden):
             v = fn(t, p)
             ref = float(g[key][i])
             assert abs(v - ref) <= 1e-13 * max(1.0, abs(ref)), (key, i, v, ref)
+
+
+def test_host_pipeline_matches_device_path(bg):
+    """Large numpy batches take the chunked pinned pipeline; same bits as device tensors."""
+    import torch
+
+    from paper_2502_00356_b200 import besselk as bk
+
+    rng = np.random.default_rng(21)
+    n = bk._HOST_CHUNK * 2 + 12345
+    x = 140.0 * (1.0 - rng.random(n))
+    nu = 20.0 * (1.0 - rng.random(n))
+    x[::1001] = 0.05 * (1.0 - rng.random(x[::1001].size))
+    host = bg.bessel_k_batch(x, nu, validate=True)
+    dev = bg.bessel_k_batch(torch.from_numpy(x).cuda(), torch.from_numpy(nu).cuda())
+    assert isinstance(host.log_value, np.ndarray)
+    assert np.array_equal(host.log_value, dev.log_value.cpu().numpy())
+    assert np.array_equal(host.value, dev.value.cpu().numpy())
+    assert np.array_equal(host.path, dev.path.cpu().numpy())
+    with pytest.raises(bg.DomainError):
+        bad = x.copy()
+        bad[n - 5] = -1.0
+        bg.bessel_k_batch(bad, nu)
