@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BGK_ABI_VERSION 2
+#define BGK_ABI_VERSION 3
 
 #define BGK_OK 0
 #define BGK_ERR_INVALID (-1)     /* bad argument (null pointer, bad size, bad enum) */
@@ -102,10 +102,11 @@ typedef struct bgk_matern_plan {
   int32_t abi;      /* BGK_ABI_VERSION */
   int32_t nnodes;   /* bins + 1 */
   int32_t nbuckets; /* entries of lut[] */
-  int32_t key_base; /* u-bucket key of lut[0] (top 16 bits of the double) */
+  int32_t key_base; /* u-bucket key of lut[0]: the double's bits >> (32 + key_shift) */
   int32_t fast;     /* 1: lut path; 0: general argmax-scan path */
   int32_t m_steps;  /* Temme: floor(nu + 0.5) */
   int32_t anchor_min, anchor_max; /* range of anchor nodes used by lut[] */
+  int32_t key_shift, pad_;        /* 15: 32 buckets per octave, 16: 16 per octave */
   double sigma_sq, beta, nu, log_prefactor, h, small_x_threshold, eps_machine;
   int64_t series_cap;
   double mu, gam1, gam2, fact, gamma_1p_mu, gamma_1m_mu; /* Temme, nu-only */

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include <cuda_runtime.h>
@@ -40,16 +41,17 @@ double gamma1_host(double mu) {  // kernels.py:219-227
   return -acc;
 }
 
-// Bucket key of a positive double: its top 16 bits (sign, exponent, 4 mantissa
-// bits) -> 16 log-spaced buckets per octave.  The device computes the same
-// key with (__double2hiint(u) >> 16).
+// Bucket key of a positive double: its top 64 - 32 - shift bits (sign, exponent
+// and 20 - shift mantissa bits) -> 2^(20 - shift) log-spaced buckets per octave
+// (shift 15: 32).  The device computes the same key as __double2hiint(u) >> shift.
+thread_local int g_key_shift = 15;
 int key_of(double u) {
   uint64_t b;
   std::memcpy(&b, &u, 8);
-  return (int)(b >> 48);
+  return (int)(b >> (32 + g_key_shift));
 }
 double u_of_key(int key) {
-  uint64_t b = (uint64_t)(uint32_t)key << 48;
+  uint64_t b = (uint64_t)(uint32_t)key << (32 + g_key_shift);
   double u;
   std::memcpy(&u, &b, 8);
   return u;
@@ -84,16 +86,30 @@ Window window_at(const bgk_matern_plan &P, double u) {
   return w;
 }
 
-// Fill plan->lut; sets plan->fast = 0 when a safe LUT cannot be built.
+// Fill plan->lut with the finest bucket resolution that fits; plan->fast = 0 when
+// no safe LUT can be built.
+bool build_lut_at(bgk_matern_plan &P, int shift);
 void build_lut(bgk_matern_plan &P) {
+  // 16 buckets per octave measured best on B200 (the 32-per-octave table's
+  // tighter windows do not pay for its larger histogram); BGK_LUT_KEY_SHIFT=15
+  // selects it for experiments.
+  const char *env = std::getenv("BGK_LUT_KEY_SHIFT");
+  const int first = (env && std::atoi(env) == 15) ? 15 : 16;
+  for (int shift = first; shift <= 16; ++shift)
+    if (build_lut_at(P, shift)) return;
+}
+
+bool build_lut_at(bgk_matern_plan &P, int shift) {
+  g_key_shift = shift;
+  P.key_shift = shift;
   P.fast = 0;
   P.nbuckets = 1;
   P.key_base = 0;
   P.lut[0] = 0;
   const double thr = P.small_x_threshold;
-  if (!(thr > 0.0) || !std::isfinite(thr) || P.nnodes < 2) return;
+  if (!(thr > 0.0) || !std::isfinite(thr) || P.nnodes < 2) return false;
   for (int k = 0; k < P.nnodes; ++k)
-    if (!std::isfinite(P.c[k]) || !std::isfinite(P.a[k])) return;
+    if (!std::isfinite(P.c[k]) || !std::isfinite(P.a[k])) return false;
   const int kb = key_of(thr);
   // Extend the bucket range until the window at a bucket's lower edge is the
   // anchor alone; every larger u then shares that single-node window.
@@ -106,10 +122,10 @@ void build_lut(bgk_matern_plan &P) {
       if (w2.m == w.m) break;
     }
     ++kt;
-    if (kt - kb + 1 > BGK_MATERN_MAX_BUCKETS) return;
+    if (kt - kb + 1 > BGK_MATERN_MAX_BUCKETS) return false;
   }
   const int nb = kt - kb + 1;
-  if (nb > BGK_MATERN_MAX_BUCKETS) return;
+  if (nb > BGK_MATERN_MAX_BUCKETS) return false;
   const int S = 9;  // samples per bucket (endpoints + 7 interior, geometric)
   for (int b = 0; b < nb; ++b) {
     const double ulo = (b == 0) ? thr : u_of_key(kb + b);
@@ -131,10 +147,10 @@ void build_lut(bgk_matern_plan &P) {
       const double ga = P.a[anchor] - u * P.c[anchor];
       for (int k = lo; k <= hi; ++k) {
         const double y = (P.aw[k] - u * P.c[k]) - ga;
-        if (!(y > -700.0 && y < 30.0)) return;
+        if (!(y > -700.0 && y < 30.0)) return false;
       }
     }
-    if (last && lo != hi) return;
+    if (last && lo != hi) return false;
     P.lut[b] = (uint32_t)anchor | ((uint32_t)lo << 10) | ((uint32_t)hi << 20);
   }
   // The kernel reads a sorted warp's common/union window from its first and
@@ -155,13 +171,13 @@ void build_lut(bgk_matern_plan &P) {
     const double ulo = (b == 0) ? thr : u_of_key(kb + b);
     const double uhi = (b == nb - 1) ? ulo : std::nextafter(u_of_key(kb + b + 1), 0.0);
     const int anchor = P.lut[b] & 1023, lo = (P.lut[b] >> 10) & 1023, hi = P.lut[b] >> 20;
-    if (b == nb - 1 && lo != hi) return;
+    if (b == nb - 1 && lo != hi) return false;
     for (int e = 0; e < 2; ++e) {
       const double u = e ? uhi : ulo;
       const double ga = P.a[anchor] - u * P.c[anchor];
       for (int k = lo; k <= hi; ++k) {
         const double y = (P.aw[k] - u * P.c[k]) - ga;
-        if (!(y > -700.0 && y < 30.0)) return;
+        if (!(y > -700.0 && y < 30.0)) return false;
       }
     }
   }
@@ -175,6 +191,7 @@ void build_lut(bgk_matern_plan &P) {
   P.nbuckets = nb;
   P.key_base = kb;
   P.fast = 1;
+  return true;
 }
 
 int check_cfg(const bgk_config *cfg) {

@@ -87,8 +87,8 @@ def test_plan_tables_match_oracle_caller(oracle, nu):
     assert p.m_steps == math.floor(nu + 0.5)
 
 
-def _key(u):
-    return int(np.array([u]).view(np.uint64)[0] >> np.uint64(48))
+def _key(u, shift):
+    return int(np.array([u]).view(np.uint64)[0] >> np.uint64(32 + shift))
 
 
 @pytest.mark.parametrize("nu,bins", [(0.3, 40), (1.5, 40), (2.9, 40), (19.5, 40), (1.5, 16),
@@ -115,7 +115,7 @@ def test_lut_windows_cover_reference_windows(nu, bins):
         g = a - u * c
         ms = int(np.argmax(g))
         keep = np.nonzero(g - g[ms] > -40.0)[0]
-        b = min(max(_key(u) - p.key_base, 0), p.nbuckets - 1)
+        b = min(max(_key(u, p.key_shift) - p.key_base, 0), p.nbuckets - 1)
         w = int(lut[b])
         anc, lo, hi = w & 1023, (w >> 10) & 1023, w >> 20
         assert lo <= keep.min() and keep.max() <= hi, (u, lo, hi, keep)
