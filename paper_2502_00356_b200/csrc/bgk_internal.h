@@ -35,6 +35,7 @@ struct BgkMaternArgs {
   long long ts;           // LOWER storage tile size
   long long tile0, tile1; // LOWER tile range
   long long ntasks;
+  double inv_beta;        // 1 / beta, computed once on the host (bgk_launch_matern)
   // COV decode helpers (filled by bgk_launch_matern)
   long long nTr, nL, nR, nD;
   // LOWER decode helpers (filled by bgk_launch_matern)
