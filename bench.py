@@ -674,7 +674,8 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
             "config": WORKLOADS["bk"]["desc"], "ms_per_step": sec["ms_per_step"],
             "roofline": {"kernel": "bgk::besselk_kernel", "achieved": a2 / 1e12,
                          "peak": p64 / 1e12, "unit": "TFLOP/s", "frac": a2 / p64,
-                         "op_convention": "W = 700 FP64-pipe ops per eval (SURVEY.md 8d)"},
+                         "op_convention": "W = 700 FP64-pipe ops per eval (SURVEY.md 8d)",
+                         "traffic": ncu_traffic("besselk_kernel", "bk")},
         }
         if "e2e_s" in sec:
             line["secondary"]["e2e"] = {"value": n2 / sec["e2e_s"], "unit": "evals/s",
