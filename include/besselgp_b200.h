@@ -106,7 +106,9 @@ typedef struct bgk_matern_plan {
   int32_t fast;     /* 1: lut path; 0: general argmax-scan path */
   int32_t m_steps;  /* Temme: floor(nu + 0.5) */
   int32_t anchor_min, anchor_max; /* range of anchor nodes used by lut[] */
-  int32_t key_shift, pad_;        /* 15: 32 buckets per octave, 16: 16 per octave */
+  int32_t key_shift;     /* 15: 32 buckets per octave, 16: 16 per octave */
+  int32_t nosub_buckets; /* lut[0, nosub_buckets): every window term e^(aw_k - u c_k) has
+                            |exponent| < 690, so the kernel may sum it unanchored */
   double sigma_sq, beta, nu, log_prefactor, h, small_x_threshold, eps_machine;
   int64_t series_cap;
   double mu, gam1, gam2, fact, gamma_1p_mu, gamma_1m_mu; /* Temme, nu-only */

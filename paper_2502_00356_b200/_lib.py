@@ -62,7 +62,7 @@ class BgkMaternPlan(ctypes.Structure):
         ("anchor_min", ctypes.c_int32),
         ("anchor_max", ctypes.c_int32),
         ("key_shift", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("nosub_buckets", ctypes.c_int32),
         ("sigma_sq", ctypes.c_double),
         ("beta", ctypes.c_double),
         ("nu", ctypes.c_double),

@@ -103,6 +103,7 @@ bool build_lut_at(bgk_matern_plan &P, int shift) {
   g_key_shift = shift;
   P.key_shift = shift;
   P.fast = 0;
+  P.nosub_buckets = 0;
   P.nbuckets = 1;
   P.key_base = 0;
   P.lut[0] = 0;
@@ -181,6 +182,26 @@ bool build_lut_at(bgk_matern_plan &P, int shift) {
       }
     }
   }
+  // Absolute-form (unanchored) buckets: a prefix of the table where every window
+  // term's exponent aw_k - u c_k stays inside the table exp's range (linear in
+  // u, so the bucket's end points bound it).
+  int nosub = 0;
+  for (int b = 0; b < nb - 1; ++b) {
+    const double ulo = (b == 0) ? thr : u_of_key(kb + b);
+    const double uhi = std::nextafter(u_of_key(kb + b + 1), 0.0);
+    const int lo = (P.lut[b] >> 10) & 1023, hi = P.lut[b] >> 20;
+    bool ok = true;
+    for (int e = 0; e < 2 && ok; ++e) {
+      const double u = e ? uhi : ulo;
+      for (int k = lo; k <= hi; ++k) {
+        const double y = P.aw[k] - u * P.c[k];
+        if (!(y > -690.0 && y < 690.0)) ok = false;
+      }
+    }
+    if (!ok) break;
+    nosub = b + 1;
+  }
+  P.nosub_buckets = nosub;
   int amin = BGK_MATERN_MAX_NODES, amax = 0;
   for (int b = 0; b < nb; ++b) {
     amin = std::min(amin, (int)(P.lut[b] & 1023));

@@ -91,13 +91,26 @@ __device__ __constant__ double kLogK[8] = {
     0x1.fdf473de6af28p-22,  // 6: ln2 lo
     0.0};
 
-// Copy the 128-entry exp table and the log tables into shared memory.
+// Copy the 128-entry exp table and the log tables into shared memory.  The exp
+// table is stored "scale-compensated": entry j is 2^(j/128) with j << 13
+// subtracted from its high word.  Adding n << 13 (n = 128 q + j) to that high
+// word then yields 2^(j/128) 2^q, because n << 13 == (q << 20) + (j << 13)
+// mod 2^32: one integer op (LEA) instead of shift + mask + add.  Read entries
+// only through exp2_scaled().
 __device__ __forceinline__ void load_tables128(double *exp128, double *invc, double *logc) {
   for (int j = threadIdx.x; j < 128; j += blockDim.x) {
-    exp128[j] = kExp2Tab128[j];
+    const double v = kExp2Tab128[j];
+    exp128[j] = __hiloint2double(__double2hiint(v) - (j << 13), __double2loint(v));
     invc[j] = kInvC128[j];
     logc[j] = kLogC128[j];
   }
+}
+
+// 2^(n/128) from the scale-compensated table (load_tables128); exact for
+// n/128 in the normal range.
+__device__ __forceinline__ double exp2_scaled(const double *__restrict__ t128, int n) {
+  const double tv = t128[n & 127];
+  return __hiloint2double(__double2hiint(tv) + (n << 13), __double2loint(tv));
 }
 
 // e^y for a quadrature node, y in (-707, 700): 128-entry table, degree-4
@@ -113,8 +126,7 @@ __device__ __forceinline__ double exp_node(double y, const double *__restrict__ 
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const double e = t128[n & 127] * p;
-  return __hiloint2double(__double2hiint(e) + ((n >> 7) << 20), __double2loint(e));
+  return exp2_scaled(t128, n) * p;
 }
 
 // Variant of exp_node on a 16-entry table 2^(j/16) (= every 8th entry of the
@@ -158,8 +170,7 @@ __device__ __forceinline__ double exp_acc(double y, const double *__restrict__ t
   p = fma(p, r, 0.5);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
-  const double e = t128[n & 127] * p;
-  return __hiloint2double(__double2hiint(e) + ((n >> 7) << 20), __double2loint(e));
+  return exp2_scaled(t128, n) * p;
 }
 
 // log(x) for positive, normal, finite x: x = 2^e m, m in [1,2), table point

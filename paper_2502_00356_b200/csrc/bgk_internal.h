@@ -36,6 +36,7 @@ struct BgkMaternArgs {
   long long tile0, tile1; // LOWER tile range
   long long ntasks;
   double inv_beta;        // 1 / beta, computed once on the host (bgk_launch_matern)
+  double lp_h;            // log_prefactor + ln h (absolute-form epilogue)
   // COV decode helpers (filled by bgk_launch_matern)
   long long nTr, nL, nR, nD;
   // LOWER decode helpers (filled by bgk_launch_matern)
