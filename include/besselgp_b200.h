@@ -232,6 +232,11 @@ int bgk_abi_version(void);
 int bgk_fp64_probe(double *scratch, int64_t blocks, int iters, void *stream,
                    double *dfma_per_launch);
 
+/* Test hook for the Matern kernel's branch-free sqrt: fast[i] = the kernel's
+ * sqrt_rn_fast(x[i]) where it claims its range (NaN elsewhere), ref[i] =
+ * __dsqrt_rn(x[i]).  Device pointers. */
+int bgk_sqrt_rn_check(const double *x, int64_t n, double *fast, double *ref, void *stream);
+
 /* Number of kernel launches issued by this library since load (for bench.py's
  * gpu_launches accounting). */
 int64_t bgk_launch_count(void);

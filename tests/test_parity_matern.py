@@ -212,3 +212,33 @@ def test_nondefault_config_and_large_beta(bg, oracle):
         ref = oracle.generate_covariance(locs, 1.0, beta, 1.2, t0=cfg.t_lower, t1=cfg.t_upper,
                                          bins=cfg.bins, thr=cfg.small_x_threshold)
         assert np.max(rel_err(cov, ref)) <= TOL, cfg_kw
+
+
+def test_sqrt_rn_fast(bg):
+    """The classify pass's branch-free sqrt equals __dsqrt_rn bit for bit wherever it
+    claims its range: random squared distances of the bench configs, random binades
+    across the whole claimed range, and exact squares / perfect-square neighbours."""
+    import torch
+
+    from paper_2502_00356_b200 import _lib
+
+    rng = np.random.default_rng(7)
+    d = rng.random((1 << 20, 2)) - rng.random((1 << 20, 2))
+    parts = [
+        (d * d).sum(1),                                   # unit-square squared distances
+        ((d * 1e3) ** 2).sum(1),                          # large coordinates
+        np.ldexp(1.0 + rng.random(1 << 21), rng.integers(-960, 1020, 1 << 21)),
+        np.arange(1, 1 << 20, dtype=np.float64) ** 2,     # exact squares
+        np.nextafter(np.arange(1, 1 << 18, dtype=np.float64) ** 2, np.inf),
+        np.nextafter(np.arange(1, 1 << 18, dtype=np.float64) ** 2, 0.0),
+    ]
+    x = torch.from_numpy(np.concatenate(parts)).cuda()
+    fast = torch.empty_like(x)
+    ref = torch.empty_like(x)
+    _lib.check(_lib.lib().bgk_sqrt_rn_check(x.data_ptr(), x.numel(), fast.data_ptr(),
+                                            ref.data_ptr(), None), "bgk_sqrt_rn_check")
+    torch.cuda.synchronize()
+    claimed = ~torch.isnan(fast)
+    assert claimed.float().mean().item() > 0.99
+    assert torch.equal(fast[claimed].view(torch.int64), ref[claimed].view(torch.int64))
+    assert np.array_equal(ref.cpu().numpy().view(np.int64), np.sqrt(x.cpu().numpy()).view(np.int64))
