@@ -57,6 +57,10 @@ double u_of_key(int key) {
   return u;
 }
 
+#ifndef BGK_WINDOW_CUTOFF
+#define BGK_WINDOW_CUTOFF 40.0
+#endif
+
 struct Window {
   int m, lo, hi;
 };
@@ -78,7 +82,7 @@ Window window_at(const bgk_matern_plan &P, double u) {
   Window w{ms, ms, ms};
   for (int k = 0; k < nn; ++k) {
     double g = P.a[k] - u * P.c[k];
-    if (g - gmax > -40.0) {
+    if (g - gmax > -BGK_WINDOW_CUTOFF) {
       if (k < w.lo) w.lo = k;
       if (k > w.hi) w.hi = k;
     }
