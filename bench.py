@@ -461,6 +461,9 @@ def run_besselk(args, D: Dist) -> dict:
     torch.cuda.synchronize(dev)
     D.barrier()
     torch.cuda.synchronize(dev)
+    clocks = ClockSampler(D.device_index)
+    if D.rank == 0:
+        clocks.start()
     l0 = _lib.launch_count()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record(stream)
@@ -469,8 +472,10 @@ def run_besselk(args, D: Dist) -> dict:
     e.record(stream)
     torch.cuda.synchronize(dev)
     launches = _lib.launch_count() - l0
+    clk = clocks.stop() if D.rank == 0 else None
     ms = D.max(s.elapsed_time(e) / args.steps)
-    res = {"ms_per_step": ms, "n": n_total, "launches": launches, "x": x, "nu": nu}
+    res = {"ms_per_step": ms, "n": n_total, "launches": launches, "x": x, "nu": nu,
+           "clocks": clk}
     # e2e: public API with host numpy arrays (H2D x, nu; D2H log K and K)
     if not args.no_e2e:
         tt = []
@@ -656,6 +661,7 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
                          "frac": achieved / p64, "peak_source": fp64["how"],
                          "traffic": ncu_traffic("besselk_kernel", "bk")},
             "gpu_launches": r["launches"],
+            "clocks": r["clocks"],
         }
         if "e2e_s" in r:
             line["e2e"] = {"value": n / r["e2e_s"], "unit": "evals/s",

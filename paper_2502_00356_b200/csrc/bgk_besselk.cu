@@ -47,7 +47,7 @@
 namespace bgk {
 
 constexpr int kBkThreads = 256;
-constexpr int kBkPerThread = 4;
+constexpr int kBkPerThread = 8;
 constexpr int kBkChunk = kBkThreads * kBkPerThread;
 constexpr int kXCells = 64;   // x cells: 4 per octave from 2^-6
 constexpr int kNuCells = 48;  // nu cells: width 1/2, last one open-ended
@@ -99,13 +99,14 @@ __device__ __forceinline__ bool in_table(double x, double a) {
   return key >= 0 && key < kXCells && a * 2.0 < (double)(kNuCells - 1);
 }
 
-// Fast fixed-window quadrature (see file header).  Requires t0 >= 0 and
-// a * max(|t0|, |t1|) <= 600 so that E^{+-j} never overflows.  Called by ALL 32
-// lanes of a warp (inactive lanes sum nothing): lane i sums nodes lo_i .. hi_i
-// in ascending order, one node per loop trip, masked once its window is done.
-// Each node: s_k = E^{k-m} + q E^{m-k} carried by two running products,
-// term = s_k e^{x (c_m - c_k)} (table exp).  The value depends only on the
-// lane's own (x, nu).
+// Fast fixed-window quadrature (see file header).  Requires t0 >= 0 and an
+// element inside the window table (its window keeps every exponent above
+// -600, checked when the table is built).  Called by ALL 32 lanes of a warp:
+// lane i sums nodes lo_i .. lo_i + n_i - 1 in ascending order.  The warp runs
+// min_i n_i nodes unmasked, then masks the ragged tail; inactive lanes
+// (n = 0) compute throw-away values.  Per node: s_k = E^{k-m} + q E^{m-k} from
+// two running products, e^{y_k} = T p (table exp), acc += (s_k T) p -- 14 FP64
+// ops.  The value depends only on the lane's own (x, nu).
 __device__ __forceinline__ double fixed_window_fast(bool active, double x, double a, uint32_t w,
                                                     const BkArgs &A,
                                                     const double2 *__restrict__ cw,
@@ -116,6 +117,8 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
   const int m = active ? anchor_node(x, a, A.t0, A.h, bins) : 0;
   const int U = min((int)(w & 0xffff), bins - m), D = min((int)(w >> 16), m);
   const int lo = m - D, n = active ? U + D + 1 : 0;
+  const int nmax = __reduce_max_sync(0xffffffffu, n);
+  const int nmin = min(__reduce_min_sync(0xffffffffu, active ? n : 0x7fffffff), nmax);
   const double ta = A.t0 + (double)m * A.h;
   const double ca = cw[m].x;
   const double tlo = A.t0 + (double)lo * A.h;
@@ -125,42 +128,52 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
   const double qa = a * (ta + tlo);
   double Qs = (qa < 700.0) ? exp_acc(-qa, t128) : 0.0;  // q E^{m - lo}
   const double mx = -x, xca = x * ca;
+  const double2 *row = cw + lo;
   double acc = 0.0;
-  // two nodes per trip (one warp vote per pair); same per-lane order as one by one.
   // cw[k] = {c_k, ln w_k}: the trapezoid weight rides in the exponent.
-  for (int j = 0; __any_sync(0xffffffffu, j < n); j += 2) {
-    const double2 c0 = cw[min(lo + j, bins)], c1 = cw[min(lo + j + 1, bins)];
-    const double y0 = fmax(fma(mx, c0.x, xca), -700.0) + c0.y;
-    const double y1 = fmax(fma(mx, c1.x, xca), -700.0) + c1.y;
-    const double s0 = P + Qs;
+  auto node = [&](double2 c) {
+    const double y = fma(mx, c.x, xca) + c.y;
+    const double s = P + Qs;
     P *= E;
     Qs *= Ei;
-    const double s1 = P + Qs;
-    P *= E;
-    Qs *= Ei;
-    const double t0 = s0 * exp_node(y0, t128);
-    const double t1 = s1 * exp_node(y1, t128);
-    acc = (j < n) ? acc + t0 : acc;
-    acc = (j + 1 < n) ? acc + t1 : acc;
+    const double tt = fma(y, kExpK[0], kExpK[6]);
+    const double nd = tt - kExpK[6];
+    const int nn = __double2loint(tt);
+    const double r = fma(nd, -kExpK[1], y);
+    double q = fma(r, kExpK[3], kExpK[4]);
+    q = fma(q, r, 0.5);
+    q = fma(q, r, 1.0);
+    const double p = fma(q, r, 1.0);
+    return s * exp2_scaled(t128, nn) * p;  // (s T) p: T scaling is exact
+  };
+  int j = 0;
+#pragma unroll 2
+  for (; j < nmin; ++j) acc += node(row[j]);
+  for (; j < nmax; ++j) {
+    const double t = node(row[min(j, bins - lo)]);
+    if (j < n) acc += t;
   }
   return (a * ta - kLn2) - xca + log_fast(A.h * acc, invc, logc);
 }
 
 __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_constant__ BkArgs A) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) unsigned char bk_smem[];
   __shared__ double s_exp[128], s_invc[128], s_logc[128];
-  __shared__ double sx[kBkChunk], snu[kBkChunk];
-  __shared__ uint16_t perm[kBkChunk];
-  __shared__ uint8_t spath[kBkChunk];
   __shared__ int hist[kBuckets + 1];
   __shared__ int s_next;
-  double2 *cw = reinterpret_cast<double2 *>(smem);  // {cosh t_k, ln w_k}, bins + 1
+  // dynamic: {cosh t_k, ln w_k} (bins + 1, only when table_ok), then the chunk
+  const int ncw = A.table_ok ? A.bins + 1 : 0;
+  double2 *cw = reinterpret_cast<double2 *>(bk_smem);
+  double *sx = reinterpret_cast<double *>(bk_smem + 16 * (size_t)ncw);
+  double *snu = sx + kBkChunk;
+  uint32_t *sw = reinterpret_cast<uint32_t *>(snu + kBkChunk);  // window word per element
+  uint16_t *perm = reinterpret_cast<uint16_t *>(sw + kBkChunk);
+  uint8_t *spath = reinterpret_cast<uint8_t *>(perm + kBkChunk);  // bucket, then path
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   load_tables128(s_exp, s_invc, s_logc);
-  if (A.table_ok)
-    for (int k = tid; k <= A.bins; k += kBkThreads)
-      cw[k] = make_double2(cosh(A.t0 + (double)k * A.h), (k == 0 || k == A.bins) ? -kLn2 : 0.0);
+  for (int k = tid; k < ncw; k += kBkThreads)
+    cw[k] = make_double2(cosh(A.t0 + (double)k * A.h), (k == 0 || k == A.bins) ? -kLn2 : 0.0);
   for (int b = tid; b <= kBuckets; b += kBkThreads) hist[b] = 0;
   if (tid == 0) s_next = 0;
 
@@ -174,24 +187,34 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
   __syncthreads();
 
   const double tmax = fmax(fabs(A.t0), fabs(A.t1));
-  // window word of an element: the table cell, or the full grid outside its range
-  auto window_of = [&](double x, double a) -> uint32_t {
-    if (in_table(x, a)) return __ldg(A.win + x_cell(x) * kNuCells + nu_cell(a));
-    return (uint32_t)A.bins | ((uint32_t)A.bins << 16);
-  };
-  auto bucket_of = [&](double x, double nu) -> int {
+  const double cmax = ncw ? cw[A.bins].x : 0.0;  // cosh(t1): t0 >= 0 on the table path
+  // classify once: bucket (widest predicted windows first; series 0, general
+  // path last) and the element's window word (0: not on the fast path)
+  for (int e = tid; e < cnt; e += kBkThreads) {
+    const double x = sx[e], a = fabs(snu[e]);
     const bool series = (A.route == 1) || (A.route == 0 && x < A.thr);
-    if (series) return 0;
-    const double a = fabs(nu);
-    if (!(A.table_ok && a * tmax <= 600.0)) return kBuckets - 1;  // general path: last
-    // widest predicted windows first (they are pulled first in the compute phase)
-    const uint32_t w = window_of(x, a);
-    const int n = (int)(w & 0xffff) + (int)(w >> 16) + 1;
-    return kMaxPred - min(n, kMaxPred - 1);
-  };
-  for (int e = tid; e < cnt; e += kBkThreads) atomicAdd(&hist[bucket_of(sx[e], snu[e])], 1);
+    int b = kBuckets - 1;
+    uint32_t w = 0;
+    if (series) {
+      b = 0;
+    } else if (A.table_ok && a * tmax <= 600.0) {  // E^{+-j} cannot overflow
+      if (in_table(x, a)) {
+        w = __ldg(A.win + x_cell(x) * kNuCells + nu_cell(a));
+        if (w == 0xffffffffu) w = 0;  // cell not proven underflow-free: reference path
+      } else if (x * cmax <= 600.0) {
+        w = (uint32_t)A.bins | ((uint32_t)A.bins << 16);  // full grid, exponents >= -600
+      }
+      if (w) {
+        const int nw = (int)(w & 0xffff) + (int)(w >> 16) + 1;
+        b = kMaxPred - min(nw, kMaxPred - 1);
+      }
+    }
+    sw[e] = w;
+    spath[e] = (uint8_t)b;
+    atomicAdd(&hist[b], 1);
+  }
   __syncthreads();
-  if (warp == 0) {  // exclusive scan over kBuckets (<= 65) bins, 3 per lane
+  if (tid < 32) {  // exclusive scan over kBuckets (<= 65) bins, 3 per lane
     int v[3], local = 0;
     for (int t = 0; t < 3; ++t) {
       const int b = lane * 3 + t;
@@ -211,8 +234,7 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
     }
   }
   __syncthreads();
-  for (int e = tid; e < cnt; e += kBkThreads)
-    perm[atomicAdd(&hist[bucket_of(sx[e], snu[e])], 1)] = (uint16_t)e;
+  for (int e = tid; e < cnt; e += kBkThreads) perm[atomicAdd(&hist[spath[e]], 1)] = (uint16_t)e;
   __syncthreads();
 
   // compute in sorted order: warps pull 32-element groups from a shared counter,
@@ -227,10 +249,10 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
     const bool valid = p < cnt;
     const int e = valid ? perm[p] : 0;
     const double x = valid ? sx[e] : 1.0, nu = valid ? snu[e] : 0.0;
+    const uint32_t w = valid ? sw[e] : 0u;
     const bool series = (A.route == 1) || (A.route == 0 && x < A.thr);
     const double a = fabs(nu);
-    const bool fast = valid && !series && A.table_ok && a * tmax <= 600.0;
-    const uint32_t w = fast ? window_of(x, a) : 0u;
+    const bool fast = valid && w != 0u;
     double lk = fixed_window_fast(fast, x, a, w, A, cw, s_exp, s_invc, s_logc);
     if (!valid) continue;
     if (series) {
@@ -348,7 +370,19 @@ static void build_window_table(double t0, double t1, int bins, uint32_t *win) {
         }
       U = std::min(U + 1, bins);
       D = std::min(D + 1, bins);
-      win[xi * kNuCells + ni] = (uint32_t)U | ((uint32_t)D << 16);
+      // The fast path evaluates e^{x (c_a - c_k)} over the window without a
+      // clamp: keep the cell only if every exponent stays far inside the table
+      // exp's range on a dense sample of the cell (else: reference path).
+      bool safe = true;
+      for (int sx = 0; sx <= 8 && safe; ++sx)
+        for (int sn = 0; sn <= 8 && safe; ++sn) {
+          const double xv = lo + (hi - lo) * sx / 8.0 * 0.9999;
+          const double nv = nlo + (nhi - nlo) * sn / 8.0 * 0.9999;
+          const int m = anchor_node(xv, nv, t0, h, bins);
+          for (int k = std::max(0, m - D); k <= std::min(bins, m + U); ++k)
+            if (!(xv * (c[m] - c[k]) > -500.0)) safe = false;
+        }
+      win[xi * kNuCells + ni] = safe ? ((uint32_t)U | ((uint32_t)D << 16)) : 0xffffffffu;
     }
   }
 }
@@ -408,11 +442,12 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
       A.win = dev;
     }
   }
-  size_t smem = sizeof(double2) * (A.table_ok ? (size_t)cfg->bins + 1 : 0);
+  const size_t chunk_bytes = (size_t)bgk::kBkChunk * (8 + 8 + 4 + 2 + 1);
+  size_t smem = sizeof(double2) * (A.table_ok ? (size_t)cfg->bins + 1 : 0) + chunk_bytes;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(bgk::besselk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double2) * (kMaxTable + 1)));
+                         (int)(sizeof(double2) * (kMaxTable + 1) + chunk_bytes));
     attr_set = true;
   }
   long long grid = (n + bgk::kBkChunk - 1) / bgk::kBkChunk;

@@ -27,7 +27,7 @@ for name, ins in funcs.items():
         ta = int(tg.group(1), 16)
         body = [x for x in ins if ta <= x[0] <= a]
         nfp = sum(1 for x in body if re.search(r"\bD(FMA|ADD|MUL)\b", x[1]))
-        if ta < a and nfp >= 30 and len(body) < 100:
+        if ta < a and nfp >= int(sys.argv[2] if len(sys.argv) > 2 else 30) and len(body) < int(sys.argv[3] if len(sys.argv) > 3 else 100):
             print(f"{name}: loop {ta:#x}-{a:#x}, {len(body)} instructions, {nfp} FP64")
             for x in body:
                 print(f"  {x[0]:#06x} {x[1]}")
