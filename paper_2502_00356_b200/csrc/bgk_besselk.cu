@@ -49,6 +49,7 @@ namespace bgk {
 constexpr int kBkThreads = 256;
 constexpr int kBkPerThread = 8;
 constexpr int kBkChunk = kBkThreads * kBkPerThread;
+constexpr int kBkChunkBytes = kBkChunk * (8 + 8 + 4 + 2 + 1 + 1);  // + 1: keeps cw 16-B aligned
 constexpr int kXCells = 64;   // x cells: 4 per octave from 2^-6
 constexpr int kNuCells = 48;  // nu cells: width 1/2, last one open-ended
 constexpr int kXKeyBase = (1023 - 6) << 2;
@@ -94,6 +95,20 @@ __host__ __device__ inline int anchor_node(double x, double a, double t0, double
   return (int)fm;
 }
 
+// Device anchor: asinh(a/x) = ln(z + sqrt(z^2 + 1)) with fast fp32 intrinsics
+// (~10 instructions instead of libdevice asinhf's ~80).  It can differ from the
+// host's anchor_node only where t*/h sits within ~1e-5 of a half-integer; the
+// window table's 1-node margin covers that shift, and the anchor itself only
+// sets the scale of the sum (rounding-level effect).
+__device__ __forceinline__ int anchor_node_fast(double x, double a, double t0, double h, int bins) {
+  if (a * a <= x) return 0;
+  const float z = __fdividef((float)a, (float)x);
+  const float ts = __logf(z + sqrtf(fmaf(z, z, 1.0f)));
+  float fm = rintf((ts - (float)t0) * (float)(1.0 / h));
+  fm = fminf(fmaxf(fm, 0.0f), (float)bins);
+  return (int)fm;
+}
+
 __device__ __forceinline__ bool in_table(double x, double a) {
   const int key = (int)((uint64_t)__double_as_longlong(x) >> 50) - kXKeyBase;
   return key >= 0 && key < kXCells && a * 2.0 < (double)(kNuCells - 1);
@@ -114,7 +129,7 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
                                                     const double *__restrict__ invc,
                                                     const double *__restrict__ logc) {
   const int bins = A.bins;
-  const int m = active ? anchor_node(x, a, A.t0, A.h, bins) : 0;
+  const int m = active ? anchor_node_fast(x, a, A.t0, A.h, bins) : 0;
   const int U = min((int)(w & 0xffff), bins - m), D = min((int)(w >> 16), m);
   const int lo = m - D, n = active ? U + D + 1 : 0;
   const int nmax = __reduce_max_sync(0xffffffffu, n);
@@ -161,14 +176,15 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
   __shared__ double s_exp[128], s_invc[128], s_logc[128];
   __shared__ int hist[kBuckets + 1];
   __shared__ int s_next;
-  // dynamic: {cosh t_k, ln w_k} (bins + 1, only when table_ok), then the chunk
+  // dynamic: the chunk at fixed offsets (no pointer registers), then
+  // {cosh t_k, ln w_k} (bins + 1, only when table_ok)
   const int ncw = A.table_ok ? A.bins + 1 : 0;
-  double2 *cw = reinterpret_cast<double2 *>(bk_smem);
-  double *sx = reinterpret_cast<double *>(bk_smem + 16 * (size_t)ncw);
+  double *sx = reinterpret_cast<double *>(bk_smem);
   double *snu = sx + kBkChunk;
   uint32_t *sw = reinterpret_cast<uint32_t *>(snu + kBkChunk);  // window word per element
   uint16_t *perm = reinterpret_cast<uint16_t *>(sw + kBkChunk);
   uint8_t *spath = reinterpret_cast<uint8_t *>(perm + kBkChunk);  // bucket, then path
+  double2 *cw = reinterpret_cast<double2 *>(bk_smem + kBkChunkBytes);
 
   const int tid = threadIdx.x, lane = tid & 31;
   load_tables128(s_exp, s_invc, s_logc);
@@ -179,18 +195,26 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
 
   const long long base = (long long)blockIdx.x * kBkChunk;
   const int cnt = (int)min((long long)kBkChunk, A.n - base);
-  // coalesced staging of this CTA's elements
-  for (int e = tid; e < cnt; e += kBkThreads) {
-    sx[e] = A.x[base + e];
-    snu[e] = A.nu[base + e];
+  // coalesced staging of this CTA's elements (all loads in flight at once)
+#pragma unroll
+  for (int i = 0; i < kBkPerThread; ++i) {
+    const int e = i * kBkThreads + tid;
+    if (e < cnt) {
+      sx[e] = __ldcs(A.x + base + e);
+      snu[e] = __ldcs(A.nu + base + e);
+    }
   }
   __syncthreads();
 
   const double tmax = fmax(fabs(A.t0), fabs(A.t1));
   const double cmax = ncw ? cw[A.bins].x : 0.0;  // cosh(t1): t0 >= 0 on the table path
   // classify once: bucket (widest predicted windows first; series 0, general
-  // path last) and the element's window word (0: not on the fast path)
-  for (int e = tid; e < cnt; e += kBkThreads) {
+  // path last) and the element's window word (0: not on the fast path).
+  // Fixed trip count so the window-table loads of all 8 elements overlap.
+#pragma unroll
+  for (int i = 0; i < kBkPerThread; ++i) {
+    const int e = i * kBkThreads + tid;
+    if (e >= cnt) break;
     const double x = sx[e], a = fabs(snu[e]);
     const bool series = (A.route == 1) || (A.route == 0 && x < A.thr);
     int b = kBuckets - 1;
@@ -237,13 +261,24 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
   for (int e = tid; e < cnt; e += kBkThreads) perm[atomicAdd(&hist[spath[e]], 1)] = (uint16_t)e;
   __syncthreads();
 
-  // compute in sorted order: warps pull 32-element groups from a shared counter,
-  // widest predicted windows first.  Every lane of the warp enters the fast sum
-  // (lanes without a fast-path element sum nothing) so it runs branch-free.
+  // compute in sorted order (widest predicted windows first): warp w takes
+  // groups w, w + 8, ... statically, and the last ~2 groups per warp are pulled
+  // from a shared counter so warps that met the slow Temme / reference-path
+  // elements (first and last groups) do not hold the CTA back.  Every lane of
+  // the warp enters the fast sum (lanes without a fast-path element sum
+  // nothing) so it runs branch-free.
   const int ngroups = (cnt + 31) >> 5;
-  for (;;) {
-    int g = lane == 0 ? atomicAdd(&s_next, 1) : 0;
-    g = __shfl_sync(0xffffffffu, g, 0);
+  constexpr int kWarps = kBkThreads / 32;
+  const int nstatic = max(0, (ngroups - 2 * kWarps) / kWarps);
+  const int warp = tid >> 5;
+  for (int round = 0;; ++round) {
+    int g;
+    if (round < nstatic) {
+      g = round * kWarps + warp;
+    } else {
+      g = lane == 0 ? nstatic * kWarps + atomicAdd(&s_next, 1) : 0;
+      g = __shfl_sync(0xffffffffu, g, 0);
+    }
     if (g >= ngroups) break;
     const int p = g * 32 + lane;
     const bool valid = p < cnt;
@@ -442,7 +477,7 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
       A.win = dev;
     }
   }
-  const size_t chunk_bytes = (size_t)bgk::kBkChunk * (8 + 8 + 4 + 2 + 1);
+  const size_t chunk_bytes = (size_t)bgk::kBkChunkBytes;
   size_t smem = sizeof(double2) * (A.table_ok ? (size_t)cfg->bins + 1 : 0) + chunk_bytes;
   static bool attr_set = false;
   if (!attr_set) {

@@ -274,6 +274,32 @@ __device__ __forceinline__ double temme_series_log_c(double x, const TemmeConst 
   double l_prev = log(s0);
   if (T.m_steps == 0) return l_prev;
   double l_cur = kLn2 - log(x) + log(s1);
+  // The reference's log-space step l' = l + log(2 eta / x + e^{l_prev - l}) is
+  // the linear forward recurrence K' = (2 eta / x) K + K_prev (stable: K grows
+  // with the order) taken in logs.  Run it linearly from K_prev = 1 (scale
+  // e^{l_prev}) -- one FMA per step instead of a log and an exp -- rescaling
+  // when K grows large, and take one log at the end.  Same values to a few ulp
+  // of ln K.
+  // Overflow-safe bounds: one step grows K by at most (eta 2/x + 1) <= 2^311
+  // for x >= 2^-300 and fewer than 1000 steps, so rescaling above 2^400 keeps
+  // every intermediate finite; outside those bounds, the log-space loop.
+  if (T.m_steps > 1 && T.m_steps < 1000 && x >= 0x1p-300) {
+    const double inv2x = 2.0 / x;
+    double kp = 1.0, kc = exp(l_cur - l_prev), off = l_prev;
+    if (kc <= 0x1p400) {
+      for (int k = 1; k < T.m_steps; ++k) {
+        const double kn = fma(T.mu + (double)k, inv2x * kc, kp);
+        kp = kc;
+        kc = kn;
+        if (kc > 0x1p400) {  // rescale by an exact power of two (rare)
+          kp *= 0x1p-400;
+          kc *= 0x1p-400;
+          off += 400.0 * kLn2;
+        }
+      }
+      return off + log(kc);
+    }
+  }
   for (int k = 1; k < T.m_steps; ++k) {
     double eta = T.mu + (double)k;
     double l_next = l_cur + log(2.0 * eta / x + exp(l_prev - l_cur));

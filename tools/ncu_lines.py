@@ -8,10 +8,19 @@ import sys
 
 rep = sys.argv[1]
 topn = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+stall = None  # optional: rank by one stall reason, e.g. NCU_STALL=stall_long_sb
+import os
+stall = os.environ.get("NCU_STALL")
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 fname = None
+scol = 4
+for r in rows:
+    if len(r) > 3 and r[0] == "Line No":
+        if stall and stall in r:
+            scol = r.index(stall)
+        break
 res = []
 tot_s = tot_i = 0
 for r in rows:
@@ -22,7 +31,7 @@ for r in rows:
         continue
     if r[0] != "":
         try:
-            s, n = int(r[4]), int(r[7])
+            s, n = int(r[scol]), int(r[7])
         except ValueError:
             continue
         res.append((s, n, f"{fname}:{r[0]}", r[1][:90]))
