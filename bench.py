@@ -514,6 +514,17 @@ def ncu_traffic(kernel: str, workload: str):
         return None
 
 
+def ncu_pipe_frac(kernel: str):
+    """The kernel's measured FP64-pipe utilisation (ncu, committed summary): the
+    executed-op view of the roofline, next to the algorithmic-W `frac`."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            v = json.load(fh).get(kernel, {}).get("fp64_pipe_pct")
+        return None if v is None else v / 100.0
+    except (OSError, ValueError):
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -621,6 +632,7 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
                 "frac": achieved / p64,
                 "peak_source": fp64["how"] + f" (nominal 148x64x1.965GHz = {nominal / 1e12:.2f})",
                 "traffic": ncu_traffic("matern_kernel", workload),
+                "ncu_fp64_pipe_frac": ncu_pipe_frac("matern_kernel"),
                 "hbm_write_gbs": write_gbs,
                 "hbm_write_frac": write_gbs / hbm,
                 "units_per_launch": units_local,
@@ -659,7 +671,8 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
                          "achieved": achieved / 1e12, "peak": p64 / 1e12, "unit": "TFLOP/s",
                          "op_convention": "FP64-pipe ops, W = 700 per eval (SURVEY.md 8d)",
                          "frac": achieved / p64, "peak_source": fp64["how"],
-                         "traffic": ncu_traffic("besselk_kernel", "bk")},
+                         "traffic": ncu_traffic("besselk_kernel", "bk"),
+                         "ncu_fp64_pipe_frac": ncu_pipe_frac("besselk_kernel")},
             "gpu_launches": r["launches"],
             "clocks": r["clocks"],
         }
@@ -681,7 +694,8 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
             "roofline": {"kernel": "bgk::besselk_kernel", "achieved": a2 / 1e12,
                          "peak": p64 / 1e12, "unit": "TFLOP/s", "frac": a2 / p64,
                          "op_convention": "W = 700 FP64-pipe ops per eval (SURVEY.md 8d)",
-                         "traffic": ncu_traffic("besselk_kernel", "bk")},
+                         "traffic": ncu_traffic("besselk_kernel", "bk"),
+                         "ncu_fp64_pipe_frac": ncu_pipe_frac("besselk_kernel")},
         }
         if "e2e_s" in sec:
             line["secondary"]["e2e"] = {"value": n2 / sec["e2e_s"], "unit": "evals/s",

@@ -50,9 +50,17 @@ constexpr int kBkThreads = 256;
 constexpr int kBkPerThread = 8;
 constexpr int kBkChunk = kBkThreads * kBkPerThread;
 constexpr int kBkChunkBytes = kBkChunk * (8 + 8 + 4 + 2 + 1 + 1);  // + 1: keeps cw 16-B aligned
-constexpr int kXCells = 64;   // x cells: 4 per octave from 2^-6
-constexpr int kNuCells = 48;  // nu cells: width 1/2, last one open-ended
-constexpr int kXKeyBase = (1023 - 6) << 2;
+#ifndef BGK_BK_XBITS
+#define BGK_BK_XBITS 2  // window table: 2^XBITS x cells per octave
+#endif
+#ifndef BGK_BK_NUSTEP
+#define BGK_BK_NUSTEP 2  // window table: nu cells per unit of nu
+#endif
+constexpr int kXBits = BGK_BK_XBITS;
+constexpr int kXCells = 16 << kXBits;             // x cells: 16 octaves from 2^-6
+constexpr int kNuStep = BGK_BK_NUSTEP;
+constexpr int kNuCells = 24 * kNuStep;            // nu cells of width 1/kNuStep, last open-ended
+constexpr int kXKeyBase = (1023 - 6) << kXBits;
 constexpr int kMaxPred = 63;  // predicted window size (sort key), clamped
 constexpr int kBuckets = kMaxPred + 2;  // + series bucket
 
@@ -78,11 +86,11 @@ __host__ __device__ inline int x_cell(double x) {
 #else
   std::memcpy(&b, &x, 8);
 #endif
-  const int key = (int)(b >> 50) - kXKeyBase;  // exponent + top 2 mantissa bits
+  const int key = (int)(b >> (52 - kXBits)) - kXKeyBase;  // exponent + top mantissa bits
   return key < 0 ? 0 : (key >= kXCells ? kXCells - 1 : key);
 }
 __host__ __device__ inline int nu_cell(double a) {
-  const double c = a * 2.0;
+  const double c = a * (double)kNuStep;
   return c >= (double)(kNuCells - 1) ? kNuCells - 1 : (int)c;
 }
 
@@ -110,8 +118,8 @@ __device__ __forceinline__ int anchor_node_fast(double x, double a, double t0, d
 }
 
 __device__ __forceinline__ bool in_table(double x, double a) {
-  const int key = (int)((uint64_t)__double_as_longlong(x) >> 50) - kXKeyBase;
-  return key >= 0 && key < kXCells && a * 2.0 < (double)(kNuCells - 1);
+  const int key = (int)((uint64_t)__double_as_longlong(x) >> (52 - kXBits)) - kXKeyBase;
+  return key >= 0 && key < kXCells && a * (double)kNuStep < (double)(kNuCells - 1);
 }
 
 // Fast fixed-window quadrature (see file header).  Requires t0 >= 0 and an
@@ -388,11 +396,12 @@ static void build_window_table(double t0, double t1, int bins, uint32_t *win) {
   for (int k = 0; k <= bins; ++k) c[k] = std::cosh(t0 + k * h);
   for (int xi = 0; xi < kXCells; ++xi) {
     const int key = xi + kXKeyBase;
-    const double lo = std::ldexp(1.0 + (key & 3) / 4.0, (key >> 2) - 1023);
-    const double hi = std::ldexp(1.0 + ((key & 3) + 1) / 4.0, (key >> 2) - 1023);
+    const int sub = 1 << kXBits;
+    const double lo = std::ldexp(1.0 + (double)(key & (sub - 1)) / sub, (key >> kXBits) - 1023);
+    const double hi = std::ldexp(1.0 + (double)((key & (sub - 1)) + 1) / sub, (key >> kXBits) - 1023);
     for (int ni = 0; ni < kNuCells; ++ni) {
-      const double nlo = ni * 0.5;
-      const double nhi = nlo + 0.5;
+      const double nlo = ni / (double)kNuStep;
+      const double nhi = nlo + 1.0 / kNuStep;
       int U = 0, D = 0;
       for (int sx = 0; sx <= 4; ++sx)
         for (int sn = 0; sn <= 4; ++sn) {
