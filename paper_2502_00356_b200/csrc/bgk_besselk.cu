@@ -309,10 +309,15 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
     spath[e] = series ? 0 : 1;
   }
   __syncthreads();
-  for (int e = tid; e < cnt; e += kBkThreads) {
-    A.log_k[base + e] = sx[e];
-    if (A.k) A.k[base + e] = snu[e];
-    if (A.path) A.path[base + e] = spath[e];
+  // coalesced streaming stores, fixed trip count (all of a thread's stores in flight)
+#pragma unroll
+  for (int i = 0; i < kBkPerThread; ++i) {
+    const int e = i * kBkThreads + tid;
+    if (e < cnt) {
+      __stcs(A.log_k + base + e, sx[e]);
+      if (A.k) __stcs(A.k + base + e, snu[e]);
+      if (A.path) A.path[base + e] = spath[e];
+    }
   }
 }
 
