@@ -77,6 +77,7 @@ struct BkArgs {
   int route;
   int table_ok;  // 1: c table fits in shared memory and t0 >= 0 -> fast path allowed
   const uint32_t *win;  // device: per (x, nu) cell, U | D << 16 (window above / below anchor)
+  const double2 *cwg;   // device: {cosh t_k, ln w_k}, k = 0..bins (host glibc cosh, as numba)
 };
 
 __host__ __device__ inline int x_cell(double x) {
@@ -196,8 +197,7 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
 
   const int tid = threadIdx.x, lane = tid & 31;
   load_tables128(s_exp, s_invc, s_logc);
-  for (int k = tid; k < ncw; k += kBkThreads)
-    cw[k] = make_double2(cosh(A.t0 + (double)k * A.h), (k == 0 || k == A.bins) ? -kLn2 : 0.0);
+  for (int k = tid; k < ncw; k += kBkThreads) cw[k] = __ldg(A.cwg + k);
   for (int b = tid; b <= kBuckets; b += kBkThreads) hist[b] = 0;
   if (tid == 0) s_next = 0;
 
@@ -446,7 +446,8 @@ static void build_window_table(double t0, double t1, int bins, uint32_t *win) {
 struct PredEntry {
   double t0, t1;
   long long bins;
-  uint32_t *dev;
+  uint32_t *dev;  // window table, then the {cosh t_k, ln w_k} node table
+  double2 *cw;
 };
 
 int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
@@ -472,13 +473,28 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
   const int64_t kMaxTable = 8191;  // 128 KB of shared memory ({c, ln w} pairs)
   A.table_ok = (cfg->t_lower >= 0.0 && cfg->bins <= kMaxTable) ? 1 : 0;
   A.win = nullptr;
+  A.cwg = nullptr;
   if (A.table_ok) {
     std::lock_guard<std::mutex> lock(mu);
     for (const PredEntry &e : cache)
-      if (e.t0 == cfg->t_lower && e.t1 == cfg->t_upper && e.bins == cfg->bins) A.win = e.dev;
+      if (e.t0 == cfg->t_lower && e.t1 == cfg->t_upper && e.bins == cfg->bins) {
+        A.win = e.dev;
+        A.cwg = e.cw;
+      }
     if (!A.win) {
-      std::vector<uint32_t> host(bgk::kXCells * bgk::kNuCells);
-      bgk::build_window_table(cfg->t_lower, cfg->t_upper, (int)cfg->bins, host.data());
+      const size_t nwin = (size_t)bgk::kXCells * bgk::kNuCells;
+      const size_t nwin_pad = (nwin + 3) & ~(size_t)3;  // 16-byte aligned node table
+      const int bins = (int)cfg->bins;
+      std::vector<uint32_t> host(nwin_pad + 4 * (size_t)(bins + 1), 0u);
+      bgk::build_window_table(cfg->t_lower, cfg->t_upper, bins, host.data());
+      // node table exactly as the reference's caller builds it: t_k = t0 + k h,
+      // cosh via the host libm (what numba calls), trapezoid weight in the exponent
+      const double h = (cfg->t_upper - cfg->t_lower) / (double)bins;
+      double *cwh = reinterpret_cast<double *>(host.data() + nwin_pad);
+      for (int k = 0; k <= bins; ++k) {
+        cwh[2 * k] = std::cosh(cfg->t_lower + (double)k * h);
+        cwh[2 * k + 1] = (k == 0 || k == bins) ? -0.6931471805599453 : 0.0;
+      }
       uint32_t *dev = nullptr;
       const size_t bytes = host.size() * sizeof(uint32_t);
       cudaError_t err = cudaMalloc(&dev, bytes);
@@ -487,8 +503,10 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
         bgk_set_error("besselk prediction table upload: %s", cudaGetErrorString(err));
         return BGK_ERR_CUDA;
       }
-      cache.push_back({cfg->t_lower, cfg->t_upper, cfg->bins, dev});
+      double2 *cwd = reinterpret_cast<double2 *>(dev + nwin_pad);
+      cache.push_back({cfg->t_lower, cfg->t_upper, cfg->bins, dev, cwd});
       A.win = dev;
+      A.cwg = cwd;
     }
   }
   const size_t chunk_bytes = (size_t)bgk::kBkChunkBytes;
