@@ -77,7 +77,7 @@ struct BkArgs {
   int route;
   int table_ok;  // 1: c table fits in shared memory and t0 >= 0 -> fast path allowed
   const uint32_t *win;  // device: per (x, nu) cell, U | D << 16 (window above / below anchor)
-  const double2 *cwg;   // device: {cosh t_k, ln w_k}, k = 0..bins (host glibc cosh, as numba)
+  const double2 *cwg;   // device: {cosh t_k, weight exponent adjust}, k = 0..bins (host libm cosh)
 };
 
 __host__ __device__ inline int x_cell(double x) {
@@ -154,9 +154,11 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
   const double mx = -x, xca = x * ca;
   const double2 *row = cw + lo;
   double acc = 0.0;
-  // cw[k] = {c_k, ln w_k}: the trapezoid weight rides in the exponent.
+  // cw[k] = {c_k, weight}: the trapezoid weight 1/2 at k = 0 and k = bins is an
+  // exponent-field adjustment (-1 << 20, in the low word of .y) added to the
+  // table value's high word -- an exact halving, no FP64 op per node.
   auto node = [&](double2 c) {
-    const double y = fma(mx, c.x, xca) + c.y;
+    const double y = fma(mx, c.x, xca);
     const double s = P + Qs;
     P *= E;
     Qs *= Ei;
@@ -168,7 +170,10 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
     q = fma(q, r, 0.5);
     q = fma(q, r, 1.0);
     const double p = fma(q, r, 1.0);
-    return s * exp2_scaled(t128, nn) * p;  // (s T) p: T scaling is exact
+    const double tv = t128[nn & 127];
+    const double T = __hiloint2double(__double2hiint(tv) + (nn << 13) + __double2loint(c.y),
+                                      __double2loint(tv));
+    return s * T * p;  // (s T) p: T scaling is exact
   };
   int j = 0;
 #pragma unroll 2
@@ -493,7 +498,9 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
       double *cwh = reinterpret_cast<double *>(host.data() + nwin_pad);
       for (int k = 0; k <= bins; ++k) {
         cwh[2 * k] = std::cosh(cfg->t_lower + (double)k * h);
-        cwh[2 * k + 1] = (k == 0 || k == bins) ? -0.6931471805599453 : 0.0;
+        // weight 1/2 at the ends as an exponent adjustment (see fixed_window_fast)
+        const uint64_t wbits = (k == 0 || k == bins) ? (uint64_t)(uint32_t)(-(1 << 20)) : 0u;
+        std::memcpy(&cwh[2 * k + 1], &wbits, 8);
       }
       uint32_t *dev = nullptr;
       const size_t bytes = host.size() * sizeof(uint32_t);
