@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define BGK_ABI_VERSION 3
+#define BGK_ABI_VERSION 4
 
 #define BGK_OK 0
 #define BGK_ERR_INVALID (-1)     /* bad argument (null pointer, bad size, bad enum) */
@@ -109,6 +109,10 @@ typedef struct bgk_matern_plan {
   int32_t key_shift;     /* 15: 32 buckets per octave, 16: 16 per octave */
   int32_t nosub_buckets; /* lut[0, nosub_buckets): every window term e^(aw_k - u c_k) has
                             |exponent| < 690, so the kernel may sum it unanchored */
+  int32_t pow_mode;      /* 0: u^nu as exp(nu ln u); else 2 nu = 2k + half is a small integer:
+                            pow_mode = 1 + 2k + half, u^nu = u^k (sqrt u)^half */
+  int32_t pad_;
+  double pow_pref;       /* exp(log_prefactor) h, normal (pow_mode != 0 only) */
   double sigma_sq, beta, nu, log_prefactor, h, small_x_threshold, eps_machine;
   int64_t series_cap;
   double mu, gam1, gam2, fact, gamma_1p_mu, gamma_1m_mu; /* Temme, nu-only */

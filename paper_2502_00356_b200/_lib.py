@@ -17,7 +17,7 @@ LIB_NAME = "libbesselgp_sm100a.so"
 LIB_PATH = os.path.join(_HERE, LIB_NAME)
 
 BGK_OK = 0
-BGK_ABI_VERSION = 3
+BGK_ABI_VERSION = 4
 ROUTE_HYBRID, ROUTE_SERIES, ROUTE_INTEGRAL = 0, 1, 2
 PATH_SERIES, PATH_INTEGRAL = 0, 1
 LAYOUT_ROW_MAJOR, LAYOUT_COL_MAJOR = 0, 1
@@ -63,6 +63,9 @@ class BgkMaternPlan(ctypes.Structure):
         ("anchor_max", ctypes.c_int32),
         ("key_shift", ctypes.c_int32),
         ("nosub_buckets", ctypes.c_int32),
+        ("pow_mode", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
+        ("pow_pref", ctypes.c_double),
         ("sigma_sq", ctypes.c_double),
         ("beta", ctypes.c_double),
         ("nu", ctypes.c_double),

@@ -341,6 +341,19 @@ int bgk_matern_plan_init_tables(bgk_matern_plan *plan, double sigma_sq, double b
   P.gam2 = 0.5 * (1.0 / P.gamma_1m_mu + 1.0 / P.gamma_1p_mu);
   P.fact = (std::fabs(P.mu) < 1e-10) ? 1.0 : P.mu * M_PI / std::sin(P.mu * M_PI);
   build_lut(P);
+  // u^nu without a log/exp pair when 2 nu is a small integer (the common GP
+  // smoothness values 1/2, 1, 3/2, 2, 5/2, ...): u^k (sqrt u)^half.
+  P.pow_mode = 0;
+  P.pow_pref = 0.0;
+  const double two_nu = 2.0 * nu;
+  if (two_nu == std::floor(two_nu) && two_nu >= 1.0 && two_nu <= 16.0) {
+    const double pref = std::exp(log_prefactor) * h;
+    if (std::isfinite(pref) && pref >= 0x1p-900 && pref <= 0x1p900) {
+      const int k = (int)std::floor(nu), half = (int)two_nu - 2 * k;
+      P.pow_mode = 1 + 2 * k + half;
+      P.pow_pref = pref;
+    }
+  }
   return BGK_OK;
 }
 
