@@ -219,9 +219,38 @@ def _validate_batch(xd, nud, cfg, route):
 _HOST_CHUNK = 1 << 22  # elements per pipelined chunk for host (numpy) batches
 
 
+_STAGE: dict = {}  # per device: two pinned staging slots (x, nu) of _HOST_CHUNK elements
+_POOL = None       # host threads for the pageable -> pinned copies (numpy releases the GIL)
+_COPY_THREADS = 8
+
+
+def _stage_slots(torch, dev):
+    slots = _STAGE.get(dev.index)
+    if slots is None:
+        slots = [(torch.empty(_HOST_CHUNK, dtype=torch.float64, pin_memory=True),
+                  torch.empty(_HOST_CHUNK, dtype=torch.float64, pin_memory=True))
+                 for _ in range(2)]
+        _STAGE[dev.index] = slots
+    return slots
+
+
+def _par_copy(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[:] = src with several host threads (pageable -> pinned is memcpy-bound)."""
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=_COPY_THREADS)
+    n = src.size
+    step = max(1 << 16, -(-n // _COPY_THREADS))
+    futs = [_POOL.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
+    for f in futs:
+        f.result()
+
+
 def _bessel_k_host_pipelined(xa, na, cfg, route, validate):
-    """Host arrays in / host arrays out, chunked so that the H2D copy of chunk i+1,
-    the kernel on chunk i and the D2H of chunk i-1 overlap (two streams); results
+    """Host arrays in / host arrays out, chunked so that the host-side copy of chunk
+    i+1 into a pinned staging slot, its H2D, the kernel on chunk i and the D2H of
+    chunk i-1 overlap (copy-in stream, compute stream, copy-out stream); results
     land directly in page-locked output arrays."""
     torch = _torch()
     _lib.lib()
@@ -234,17 +263,30 @@ def _bessel_k_host_pipelined(xa, na, cfg, route, validate):
     out_k = torch.empty(n, dtype=torch.float64, pin_memory=True)
     out_p = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     comp = torch.cuda.current_stream(dev)
+    inp = torch.cuda.Stream(dev)
     copy = torch.cuda.Stream(dev)
-    nbuf = 2
-    bufs = [None] * nbuf
-    freed = [None] * nbuf
+    slots = _stage_slots(torch, dev)
+    staged = [None, None]  # event: the slot's H2D has finished (slot reusable)
+    freed = [None, None]   # event: the chunk's D2H has finished (device buffers reusable)
     for ci, c0 in enumerate(range(0, n, _HOST_CHUNK)):
         c1 = min(n, c0 + _HOST_CHUNK)
-        s = ci % nbuf
-        if freed[s] is not None:
-            comp.wait_event(freed[s])
-        xd = torch.from_numpy(xf[c0:c1]).to(dev, non_blocking=True)
-        nd = torch.from_numpy(nf[c0:c1]).to(dev, non_blocking=True)
+        s = ci % 2
+        if staged[s] is not None:
+            staged[s].synchronize()
+        sx, sn = slots[s]
+        _par_copy(sx.numpy()[:c1 - c0], xf[c0:c1])
+        _par_copy(sn.numpy()[:c1 - c0], nf[c0:c1])
+        with torch.cuda.stream(inp):
+            if freed[s] is not None:
+                inp.wait_event(freed[s])
+            xd = sx[:c1 - c0].to(dev, non_blocking=True)
+            nd = sn[:c1 - c0].to(dev, non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(inp)
+        staged[s] = ev_in
+        comp.wait_event(ev_in)
+        xd.record_stream(comp)
+        nd.record_stream(comp)
         if validate:
             _validate_batch(xd, nd, cfg, route)
         logk, k, path = _launch_besselk(xd, nd, cfg, _ROUTES[route])
@@ -261,7 +303,6 @@ def _bessel_k_host_pipelined(xa, na, cfg, route, validate):
         logk.record_stream(copy)
         k.record_stream(copy)
         path.record_stream(copy)
-        bufs[s] = (logk, k, path)
         freed[s] = ev
     copy.synchronize()
     return BatchResult(out_l.numpy().reshape(shape), out_k.numpy().reshape(shape),
