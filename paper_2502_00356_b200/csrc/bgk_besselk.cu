@@ -146,8 +146,8 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
   const double ta = A.t0 + (double)m * A.h;
   const double ca = cw[m].x;
   const double tlo = A.t0 + (double)lo * A.h;
-  const double E = exp_acc(a * A.h, t128);
-  const double Ei = exp_acc(-a * A.h, t128);
+  double E, Ei;
+  exp_pair(a * A.h, t128, E, Ei);
   double P = exp_acc(-a * (ta - tlo), t128);  // E^{lo - m}
   const double qa = a * (ta + tlo);
   double Qs = (qa < 700.0) ? exp_acc(-qa, t128) : 0.0;  // q E^{m - lo}
