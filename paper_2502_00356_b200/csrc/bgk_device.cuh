@@ -1,9 +1,9 @@
 // bgk_device.cuh -- device math shared by the BesselK and Matern kernels (sm_100a).
 //
 // Everything here is FP64.  The hot loops are bound by the FP64 pipe (64 lanes
-// per SM per clock on B200), so the per-node exponential is a table-driven
-// 2^(j/64) * poly5 scheme (10 FP64 ops, 2-3 ulp) instead of libdevice exp
-// (15 ops + range checks); rarely-hit paths (Temme series, out-of-range
+// per SM per clock on B200), so exponentials and logs are table-driven
+// (128-entry tables in shared memory, 7-11 FP64 ops) instead of libdevice exp /
+// log (15-29 ops + range checks); rarely-hit paths (Temme series, out-of-range
 // parameters) keep libdevice for robustness.
 #pragma once
 
@@ -17,60 +17,6 @@ namespace bgk {
 
 constexpr double kLn2 = 0.6931471805599453;  // kernels.py:16
 constexpr double kPi = 3.141592653589793;
-
-// 2^(j/64), j = 0..63, correctly rounded (generated with mpmath, 200 bits).
-__device__ __constant__ double kExp2Tab64[64] = {
-    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
-    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
-    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
-    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
-    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
-    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
-    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
-    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
-    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
-    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
-    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
-    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
-    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
-    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
-    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
-    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
-};
-
-// Copy the exp table into shared memory (call from all threads, then sync).
-__device__ __forceinline__ void load_exp_tab(double *tab) {
-  for (int j = threadIdx.x; j < 64; j += blockDim.x) tab[j] = kExp2Tab64[j];
-}
-
-// e^y for y in [-707, 709]: y = (64 n + j) ln2/64 + r, |r| <= ln2/128,
-// e^y = 2^n * 2^(j/64) * poly5(r).  Cody-Waite two-constant reduction; the
-// degree-5 Taylor tail is r^6/720 < 3.5e-17.  Outside the range the result is
-// garbage (callers clamp or mask).  10 FP64-pipe ops + 1 LDS + 3 integer ops.
-__device__ __forceinline__ double exp_tab(double y, const double *__restrict__ tab) {
-  const double kMagic = 0x1.8p52;
-  const double kInvL = 0x1.71547652b82fep+6;  // 64/ln2
-  const double kL1 = 0x1.62e42fefa39efp-7;    // ln2/64 (hi)
-  const double kL2 = 0x1.abc9e3b39803fp-62;   // ln2/64 (lo)
-  double t = fma(y, kInvL, kMagic);
-  double nd = t - kMagic;
-  int n = __double2loint(t);
-  double r = fma(nd, -kL1, y);
-  r = fma(nd, -kL2, r);
-  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  double e = tab[n & 63] * p;
-  int hi = __double2hiint(e) + ((n >> 6) << 20);
-  return __hiloint2double(hi, __double2loint(e));
-}
-
-// Full-range e^y (any finite y, inf/0 on overflow/underflow like exp()).
-__device__ __forceinline__ double exp_full(double y, const double *__restrict__ tab) {
-  return (fabs(y) < 700.0) ? exp_tab(y, tab) : exp(y);
-}
 
 // ---------------------------------------------------------------------------------
 // 128-entry table exp / log.  Coefficients live in __constant__ memory so DFMA
@@ -127,35 +73,6 @@ __device__ __forceinline__ double exp_node(double y, const double *__restrict__ 
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   return exp2_scaled(t128, n) * p;
-}
-
-// Variant of exp_node on a 16-entry table 2^(j/16) (= every 8th entry of the
-// 128 table): each 8-byte entry owns one shared-memory bank pair, so a warp's
-// lookups never conflict (the 128-entry table costs ~3 wavefronts per
-// half-warp).  Degree-6 polynomial on |r| <= ln2/32 (truncation 4.4e-16),
-// one-constant reduction.  9 FP64 ops + LDS + 4 integer ops.
-__device__ __constant__ double kExp16K[3] = {
-    0x1.71547652b82fep+4,  // 16/ln2
-    0x1.62e42fefa39efp-5,  // ln2/16
-    1.0 / 720.0};
-
-__device__ __forceinline__ void load_exp16(double *t16) {
-  for (int j = threadIdx.x; j < 16; j += blockDim.x) t16[j] = kExp2Tab128[8 * j];
-}
-
-__device__ __forceinline__ double exp_node16(double y, const double *__restrict__ t16) {
-  const double t = fma(y, kExp16K[0], kExpK[6]);
-  const double nd = t - kExpK[6];
-  const int n = __double2loint(t);
-  const double r = fma(nd, -kExp16K[1], y);
-  double p = fma(r, kExp16K[2], kExpK[5]);
-  p = fma(p, r, kExpK[3]);
-  p = fma(p, r, kExpK[4]);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
-  const double e = t16[n & 15] * p;
-  return __hiloint2double(__double2hiint(e) + ((n >> 4) << 20), __double2loint(e));
 }
 
 // e^y to ~2 ulp for |y| < 700 (two-constant reduction, degree 5).
