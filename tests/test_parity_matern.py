@@ -242,3 +242,38 @@ def test_sqrt_rn_fast(bg):
     assert claimed.float().mean().item() > 0.99
     assert torch.equal(fast[claimed].view(torch.int64), ref[claimed].view(torch.int64))
     assert np.array_equal(ref.cpu().numpy().view(np.int64), np.sqrt(x.cpu().numpy()).view(np.int64))
+
+
+@pytest.mark.parametrize("nu", [0.5, 1.0, 1.5, 2.5, 7.5])
+def test_pow_mode_matches_general_power(bg, oracle, nu):
+    """Half-integer / integer nu plans take u^nu = u^k sqrt(u)^half (pow_mode); the same
+    plan with pow_mode cleared takes exp(nu ln u).  Both agree to rounding and both
+    match the oracle; the three kernel paths of a plan (fast group, per-lane, mirror)
+    stay bitwise symmetric."""
+    import ctypes
+
+    import torch
+
+    from paper_2502_00356_b200 import _lib
+    from paper_2502_00356_b200.covariance import _cov_launch, matern_plan
+
+    rng = np.random.default_rng(11)
+    N = 700
+    locs = rng.random((N, 2))
+    theta = bg.MaternParams(1.7, 0.1, nu)
+    plan = matern_plan(theta)
+    assert plan.pow_mode != 0
+    general = _lib.BgkMaternPlan()
+    ctypes.memmove(ctypes.byref(general), ctypes.byref(plan), ctypes.sizeof(plan))
+    general.pow_mode = 0
+    lxy = torch.from_numpy(np.ascontiguousarray(locs.T)).cuda()
+    outs = []
+    for p in (plan, general):
+        out = torch.empty((N, N), dtype=torch.float64, device="cuda")
+        _cov_launch(p, lxy[0], lxy[1], N, 0, N, out, N, _lib.LAYOUT_ROW_MAJOR)
+        outs.append(out.cpu().numpy())
+    fast, gen = outs
+    assert np.array_equal(fast, fast.T) and np.array_equal(gen, gen.T)
+    assert np.max(rel_err(fast, gen)) <= 1e-13
+    ref = oracle.generate_covariance(locs, 1.7, 0.1, nu)
+    assert np.max(rel_err(fast, ref)) <= TOL
