@@ -35,6 +35,7 @@ struct BgkMaternArgs {
   long long ts;           // LOWER storage tile size
   long long tile0, tile1; // LOWER tile range
   long long ntasks;
+  unsigned long long *task_counter;  // persistent variant only (BGK_MATERN_PERSISTENT)
   double inv_beta;        // 1 / beta, computed once on the host (bgk_launch_matern)
   double lp_h;            // log_prefactor + ln h (absolute-form epilogue)
   // COV decode helpers (filled by bgk_launch_matern)
