@@ -304,7 +304,7 @@ def run_matern(args, D: Dist) -> dict:
             from paper_2502_00356_b200.distributed import MACRO, PeerMatrix
 
             try:
-                pm = PeerMatrix(N, device=dev)
+                pm = PeerMatrix(N, device=dev, mode=args.peer_layout)
                 mode = "peer"
             except Exception as ex:  # noqa: BLE001 -- fall back to no-communication rows
                 log(f"peer mapping unavailable ({ex}); using independent row blocks")
@@ -312,6 +312,11 @@ def run_matern(args, D: Dist) -> dict:
                     raise
         if pm is not None:
             r0, r1, out = pm.r0, pm.r1, pm.block
+        if pm is not None and pm.mode == "band":
+            from paper_2502_00356_b200.distributed import band_computed_entries
+
+            computed_local = float(band_computed_entries(N, D.world, D.rank))
+        elif pm is not None:
             lt = np.arange(*pm.tiles, dtype=np.int64)
             pp = ((np.sqrt(8.0 * lt + 1.0) - 1.0) // 2).astype(np.int64)
             pp += ((pp + 1) * (pp + 2) // 2 <= lt)
@@ -533,6 +538,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="m100")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--peer-layout", choices=["band", "tiles"], default="band",
+                    help="peer mode work split: each rank's cyclic half band of its own rows "
+                         "(direct stores local, mirrors over NVLink) or equal lower-tile ranges")
     ap.add_argument("--mode", choices=["auto", "peer", "rows"], default="auto",
                     help="N>1 full-matrix sharding: fused P2P mirror stores (peer) or "
                          "independent row blocks (rows); auto = peer with fallback")
@@ -616,7 +624,8 @@ def build_line(args, world, wl, matern, r, sec, peaks, fp64):
                        "sigma2": 1.0, "beta": 0.1, "bins": 40, "t_window": [0.0, 9.0],
                        "parallelism": (f"packed lower-tile shards x{world}" if workload == "m200" else
                                        f"fused compute + NVLink P2P mirror stores x{world}: each "
-                                       "lower 64x64 tile computed once" if r.get("mode") == "peer"
+                                       f"64x64 tile pair computed once ({args.peer_layout} layout)"
+                                       if r.get("mode") == "peer"
                                        else f"row-block shards x{world}, no collective"),
                        "l2": "output matrix (80 GB at N=100K) >> 126 MB L2; every step rewrites it"},
             "entries_per_s": r["stored_entries"] * len(nus) / t,

@@ -216,6 +216,20 @@ int bgk_matern_covariance_peer(const bgk_matern_plan *plan, const double *lx, co
                                double *const *bases, int64_t tile_begin, int64_t tile_end,
                                void *stream);
 
+/* The same matrix with an owner-computes assignment ("cyclic half band"): owner
+ * `rank` computes, for each of its macro rows p, the tiles (p, q) with
+ * q = p - d (mod T), d = 0 .. floor(T/2) (d = T/2, T even, only for p < T/2).
+ * Every unordered tile pair is computed exactly once across the ranks and the
+ * work is balanced for equal row blocks, as with bgk_matern_covariance_peer, but
+ * every direct store lands in the rank's own block: only the mirrors cross
+ * NVLink, half the peer traffic of the lower-triangle ranges.  Upper tiles
+ * (q > p) are computed directly; entries are pure functions of the location
+ * pair, so the matrix is bitwise the same. */
+int bgk_matern_covariance_peer_band(const bgk_matern_plan *plan, const double *lx,
+                                    const double *ly, int64_t N, int G,
+                                    const int64_t *macro_row_start, double *const *bases,
+                                    int rank, void *stream);
+
 /* CUDA IPC for one-process-per-GPU peer mapping.  export: handle (64 bytes) of the
  * allocation holding ptr and ptr's offset in it.  open: map a peer's allocation on
  * the current device and return base + offset.  close: unmap (pass the pointer

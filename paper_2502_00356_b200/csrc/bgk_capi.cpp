@@ -444,41 +444,87 @@ int bgk_matern_lower_tiles(const bgk_matern_plan *plan, const double *lx, const 
   return bgk_launch_matern(plan, A, BGK_MODE_LOWER, (cudaStream_t)stream);
 }
 
-int bgk_matern_covariance_peer(const bgk_matern_plan *plan, const double *lx, const double *ly,
-                               int64_t N, int G, const int64_t *macro_row_start,
-                               double *const *bases, int64_t tile_begin, int64_t tile_end,
-                               void *stream) {
-  if (int rc = check_plan(plan)) return rc;
+namespace {
+// shared argument checks of the two peer entry points
+int check_peer_owners(const char *what, int64_t N, int G, const int64_t *macro_row_start,
+                      double *const *bases) {
   const int64_t T = (N + BGK_MACRO_TILE - 1) / BGK_MACRO_TILE;
-  const int64_t total = T * (T + 1) / 2;
-  if (N < 0 || G < 1 || G > BGK_MAX_PEERS || !macro_row_start || !bases || tile_begin < 0 ||
-      tile_end > total || tile_begin > tile_end) {
-    bgk_set_error("bgk_matern_covariance_peer: bad N/G/tile range");
+  if (N < 0 || G < 1 || G > BGK_MAX_PEERS || !macro_row_start || !bases) {
+    bgk_set_error("%s: bad N/G", what);
     return BGK_ERR_INVALID;
   }
   if (macro_row_start[0] != 0 || macro_row_start[G] != T) {
-    bgk_set_error("bgk_matern_covariance_peer: macro_row_start must run from 0 to ceil(N/64)");
+    bgk_set_error("%s: macro_row_start must run from 0 to ceil(N/64)", what);
     return BGK_ERR_INVALID;
   }
   for (int h = 0; h < G; ++h) {
     const bool empty = macro_row_start[h + 1] == macro_row_start[h];
     if (macro_row_start[h + 1] < macro_row_start[h] || (!bases[h] && !empty)) {
-      bgk_set_error("bgk_matern_covariance_peer: bad owner %d", h);
+      bgk_set_error("%s: bad owner %d", what, h);
       return BGK_ERR_INVALID;
     }
+  }
+  return BGK_OK;
+}
+
+BgkMaternArgs peer_args(const double *lx, const double *ly, int64_t N, int G,
+                        const int64_t *macro_row_start, double *const *bases) {
+  BgkMaternArgs A{};
+  A.rx = lx; A.ry = ly; A.cx = lx; A.cy = ly; A.out = bases[0];
+  A.m = N; A.n = N; A.ld = N; A.layout = BGK_LAYOUT_ROW_MAJOR;
+  A.G = G;
+  for (int h = 0; h <= G; ++h) A.pstart[h] = macro_row_start[h];
+  for (int h = 0; h < G; ++h) A.bases[h] = bases[h];
+  return A;
+}
+}  // namespace
+
+int bgk_matern_covariance_peer(const bgk_matern_plan *plan, const double *lx, const double *ly,
+                               int64_t N, int G, const int64_t *macro_row_start,
+                               double *const *bases, int64_t tile_begin, int64_t tile_end,
+                               void *stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (int rc = check_peer_owners("bgk_matern_covariance_peer", N, G, macro_row_start, bases))
+    return rc;
+  const int64_t T = (N + BGK_MACRO_TILE - 1) / BGK_MACRO_TILE;
+  if (tile_begin < 0 || tile_end > T * (T + 1) / 2 || tile_begin > tile_end) {
+    bgk_set_error("bgk_matern_covariance_peer: bad tile range");
+    return BGK_ERR_INVALID;
   }
   if (tile_end == tile_begin || N == 0) return BGK_OK;
   if (!lx || !ly) {
     bgk_set_error("bgk_matern_covariance_peer: NULL locations");
     return BGK_ERR_INVALID;
   }
-  BgkMaternArgs A{};
-  A.rx = lx; A.ry = ly; A.cx = lx; A.cy = ly; A.out = bases[0];
-  A.m = N; A.n = N; A.ld = N; A.layout = BGK_LAYOUT_ROW_MAJOR;
+  BgkMaternArgs A = peer_args(lx, ly, N, G, macro_row_start, bases);
   A.tile0 = tile_begin; A.tile1 = tile_end;
-  A.G = G;
-  for (int h = 0; h <= G; ++h) A.pstart[h] = macro_row_start[h];
-  for (int h = 0; h < G; ++h) A.bases[h] = bases[h];
+  return bgk_launch_matern(plan, A, BGK_MODE_PEER, (cudaStream_t)stream);
+}
+
+int bgk_matern_covariance_peer_band(const bgk_matern_plan *plan, const double *lx,
+                                    const double *ly, int64_t N, int G,
+                                    const int64_t *macro_row_start, double *const *bases,
+                                    int rank, void *stream) {
+  if (int rc = check_plan(plan)) return rc;
+  if (int rc = check_peer_owners("bgk_matern_covariance_peer_band", N, G, macro_row_start, bases))
+    return rc;
+  if (rank < 0 || rank >= G) {
+    bgk_set_error("bgk_matern_covariance_peer_band: rank %d outside [0, %d)", rank, G);
+    return BGK_ERR_INVALID;
+  }
+  const int64_t T = (N + BGK_MACRO_TILE - 1) / BGK_MACRO_TILE;
+  const int64_t p0 = macro_row_start[rank], p1 = macro_row_start[rank + 1];
+  if (p1 == p0 || N == 0) return BGK_OK;
+  if (!lx || !ly) {
+    bgk_set_error("bgk_matern_covariance_peer_band: NULL locations");
+    return BGK_ERR_INVALID;
+  }
+  BgkMaternArgs A = peer_args(lx, ly, N, G, macro_row_start, bases);
+  A.band = 1;
+  A.bT = T;
+  A.bW = T / 2 + 1;  // d = 0 .. floor(T/2); for odd T that is (T - 1)/2 + 1
+  A.brow0 = p0;
+  A.tile0 = p0; A.tile1 = p1;
   return bgk_launch_matern(plan, A, BGK_MODE_PEER, (cudaStream_t)stream);
 }
 

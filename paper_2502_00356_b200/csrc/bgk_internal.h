@@ -45,6 +45,9 @@ struct BgkMaternArgs {
   // PEER: G row-block owners; owner h holds macro rows [pstart[h], pstart[h+1])
   // (rows [64 pstart[h], min(N, 64 pstart[h+1]))) at bases[h], row-major, ld = N.
   int G;
+  int band;               // 0: tiles [tile0, tile1) of the lower triangle; 1: cyclic half
+                          // band of macro rows [tile0, tile1) (= brow0 ..), bW tiles per row
+  long long brow0, bW, bT;
   long long pstart[BGK_MAX_PEERS + 1];
   double *bases[BGK_MAX_PEERS];
 };

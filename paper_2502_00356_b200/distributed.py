@@ -162,7 +162,71 @@ def peer_tile_range(N: int, world: int, rank: int) -> tuple[int, int]:
     return total * rank // world, total * (rank + 1) // world
 
 
-def _launch_peer(plan, lx, ly, N, starts, bases, l0, l1):
+PEER_MODES = ("band", "tiles")
+
+
+def band_tiles(N: int, world: int, rank: int) -> int:
+    """Macro tiles rank computes in "band" mode: for each of its macro rows p the
+    tiles q = p - d (mod T), d = 0 .. floor(T/2), d = T/2 (T even) only for p < T/2."""
+    T = -(-N // MACRO)
+    s = macro_row_starts(N, world)
+    n = 0
+    for p in range(s[rank], s[rank + 1]):
+        n += T // 2 + 1
+        if T % 2 == 0 and 2 * p >= T:
+            n -= 1
+    return n
+
+
+def band_computed_entries(N: int, world: int, rank: int) -> int:
+    """Matrix entries rank computes in "band" mode (edge tiles clipped at N)."""
+    T = -(-N // MACRO)
+    s = macro_row_starts(N, world)
+    n = 0
+    for p in range(s[rank], s[rank + 1]):
+        rp = min(MACRO, N - MACRO * p)
+        for d in range(T // 2 + 1):
+            if T % 2 == 0 and 2 * d == T and 2 * p >= T:
+                continue
+            n += rp * min(MACRO, N - MACRO * ((p - d) % T))
+    return n
+
+
+def peer_mirror_bytes(N: int, world: int, rank: int, mode: str = "band") -> int:
+    """Bytes rank stores into OTHER ranks' blocks (NVLink traffic), both modes."""
+    T = -(-N // MACRO)
+    s = macro_row_starts(N, world)
+    own = [0] * T
+    for h in range(world):
+        for p in range(s[h], s[h + 1]):
+            own[p] = h
+
+    def rows(p):
+        return min(MACRO, N - MACRO * p)
+
+    total = 0
+    if mode == "band":
+        for p in range(s[rank], s[rank + 1]):
+            for d in range(T // 2 + 1):
+                if T % 2 == 0 and 2 * d == T and 2 * p >= T:
+                    continue
+                q = (p - d) % T
+                if d and own[q] != rank:
+                    total += rows(p) * rows(q) * 8
+    else:
+        l0, l1 = peer_tile_range(N, world, rank)
+        p = 0
+        for l in range(l0, l1):
+            while (p + 1) * (p + 2) // 2 <= l:
+                p += 1
+            q = l - p * (p + 1) // 2
+            b = rows(p) * rows(q) * 8
+            total += b * (own[p] != rank) + (b if p != q and own[q] != rank else 0)
+    return total
+
+
+def _launch_peer(plan, lx, ly, N, starts, bases, l0, l1, rank=None):
+    """tiles mode: lower tiles [l0, l1); band mode (rank given): rank's cyclic half band."""
     import ctypes
 
     import torch
@@ -173,16 +237,22 @@ def _launch_peer(plan, lx, ly, N, starts, bases, l0, l1):
     G = len(bases)
     st = (ctypes.c_int64 * (G + 1))(*starts)
     bp = (ctypes.c_void_p * G)(*bases)
+    stream = torch.cuda.current_stream().cuda_stream
+    if rank is not None:
+        rc = L.bgk_matern_covariance_peer_band(ctypes.byref(plan), lx.data_ptr(), ly.data_ptr(),
+                                               N, G, st, bp, rank, stream)
+        _lib.check(rc, "bgk_matern_covariance_peer_band")
+        return
     rc = L.bgk_matern_covariance_peer(ctypes.byref(plan), lx.data_ptr(), ly.data_ptr(), N, G, st,
-                                      bp, l0, l1, torch.cuda.current_stream().cuda_stream)
+                                      bp, l0, l1, stream)
     _lib.check(rc, "bgk_matern_covariance_peer")
 
 
-def generate_covariance_peer_emulated(locs, theta, world: int, cfg=None):
+def generate_covariance_peer_emulated(locs, theta, world: int, cfg=None, mode: str = "band"):
     """Single-process check of the peer-store kernel: ``world`` owner buffers on the
-    current GPU stand in for the ranks' HBM and every rank's tile range is
-    launched here.  Returns the owners' row blocks (their concatenation is the
-    full matrix)."""
+    current GPU stand in for the ranks' HBM and every rank's share is launched
+    here.  Returns the owners' row blocks (their concatenation is the full
+    matrix)."""
     import torch
 
     from .besselk import DEFAULT_CONFIG
@@ -196,10 +266,14 @@ def generate_covariance_peer_emulated(locs, theta, world: int, cfg=None):
     for g in range(world):
         r0, r1 = owner_rows(N, world, g)
         blocks.append(torch.empty((r1 - r0, N), dtype=torch.float64, device=lx.device))
-    bases = [b.data_ptr() for b in blocks]
+    bases = [b.data_ptr() if b.numel() else 1 for b in blocks]
+    if mode not in PEER_MODES:
+        raise ValueError(f"mode must be one of {PEER_MODES}")
     for g in range(world):
-        l0, l1 = peer_tile_range(N, world, g)
-        _launch_peer(plan, lx, ly, N, starts, bases, l0, l1)
+        if mode == "band":
+            _launch_peer(plan, lx, ly, N, starts, bases, 0, 0, rank=g)
+        else:
+            _launch_peer(plan, lx, ly, N, starts, bases, *peer_tile_range(N, world, g))
     return blocks
 
 
@@ -212,7 +286,7 @@ class PeerMatrix:
     the whole matrix is complete after ``compute`` on every rank plus a barrier.
     """
 
-    def __init__(self, N: int, group=None, device=None):
+    def __init__(self, N: int, group=None, device=None, mode: str = "band"):
         import ctypes
 
         import torch
@@ -247,11 +321,19 @@ class PeerMatrix:
             self.bases.append(p.value)
             self._opened.append((p.value, o))
         self.starts = macro_row_starts(N, self.world)
+        if mode not in PEER_MODES:
+            raise ValueError(f"mode must be one of {PEER_MODES}")
+        self.mode = mode
         self.tiles = peer_tile_range(N, self.world, self.rank)
 
     def compute(self, plan, lx, ly):
-        """Launch this rank's tiles (stream-ordered; no barrier)."""
-        _launch_peer(plan, lx, ly, self.N, self.starts, self.bases, *self.tiles)
+        """Launch this rank's tiles (stream-ordered; no barrier).  "band": the cyclic
+        half band of its own macro rows (every direct store local, only mirrors
+        cross NVLink); "tiles": an equal contiguous range of lower tiles."""
+        if self.mode == "band":
+            _launch_peer(plan, lx, ly, self.N, self.starts, self.bases, 0, 0, rank=self.rank)
+        else:
+            _launch_peer(plan, lx, ly, self.N, self.starts, self.bases, *self.tiles)
 
     def close(self):
         from . import _lib
@@ -262,7 +344,7 @@ class PeerMatrix:
         self._opened = []
 
 
-def generate_covariance_peer(locs, theta, cfg=None, *, group=None, device=None):
+def generate_covariance_peer(locs, theta, cfg=None, *, group=None, device=None, mode="band"):
     """Row block of this rank, with every lower macro tile of the matrix computed
     once across the group and transposes stored straight into the owning GPU's
     memory over NVLink.  Returns (r0, r1, block); collective."""
@@ -272,7 +354,7 @@ def generate_covariance_peer(locs, theta, cfg=None, *, group=None, device=None):
     from .covariance import _coords, matern_plan
 
     lx, ly = _coords(locs)
-    pm = PeerMatrix(lx.numel(), group=group, device=device)
+    pm = PeerMatrix(lx.numel(), group=group, device=device, mode=mode)
     pm.compute(matern_plan(theta, cfg or DEFAULT_CONFIG), lx, ly)
     torch.cuda.synchronize(pm.device)
     _dist().barrier(group=group)

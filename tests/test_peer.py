@@ -19,8 +19,10 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("N,G", [(1000, 2), (1000, 3), (777, 8), (130, 5), (64, 4), (2113, 7)])
-def test_peer_emulated_union_is_full_matrix(N, G):
+@pytest.mark.parametrize("mode", ["band", "tiles"])
+@pytest.mark.parametrize("N,G", [(1000, 2), (1000, 3), (777, 8), (130, 5), (64, 4), (2113, 7),
+                                 (1024, 4), (65, 1), (200, 3)])
+def test_peer_emulated_union_is_full_matrix(N, G, mode):
     import paper_2502_00356_b200 as bg
     from paper_2502_00356_b200 import distributed as D
 
@@ -28,7 +30,7 @@ def test_peer_emulated_union_is_full_matrix(N, G):
     locs = rng.random((N, 2))
     theta = bg.MaternParams(1.0, 0.1, 1.5)
     full = bg.generate_covariance(locs, theta, device="cuda").data
-    blocks = D.generate_covariance_peer_emulated(locs, theta, G)
+    blocks = D.generate_covariance_peer_emulated(locs, theta, G, mode=mode)
     assert sum(b.shape[0] for b in blocks) == N
     assert torch.equal(torch.cat(blocks, 0), full)
 
