@@ -433,7 +433,18 @@ def run_matern(args, D: Dist) -> dict:
                 D.max(dt)
         res["e2e_s"] = statistics.median(ts_)
         res["e2e_h2d"] = float(locs.nbytes) * D.world * len(nus)
-        res["e2e_d2h"] = stored * 8.0
+        from paper_2502_00356_b200.covariance import host_d2h_bytes
+
+        res["e2e_d2h"] = float(host_d2h_bytes(N, (r0, r1))) * len(nus)
+        if r0 == 0 and r1 == N and res["e2e_d2h"] < stored * 8.0 * len(nus):
+            from paper_2502_00356_b200.covariance import _host_threads
+
+            res["e2e_how"] = (
+                "paper_2502_00356_b200.generate_covariance(numpy locs, theta, out=pinned host "
+                "array): H2D of the locations; per 1 GB row block the device computes the lower "
+                f"part, a 2D copy moves it (half the matrix over PCIe) and {_host_threads()} host "
+                "threads mirror it into the upper triangle (non-temporal stores) while the next "
+                "block computes and copies; wall clock")
         del host
     return res
 

@@ -250,6 +250,23 @@ int bgk_abi_version(void);
 int bgk_fp64_probe(double *scratch, int64_t blocks, int iters, void *stream,
                    double *dfma_per_launch);
 
+/* ---- host-side helpers of the host-buffer covariance path ----------------------------
+ * The full N x N matrix into a host array moves only the lower triangle over PCIe
+ * (rows [b0, b1) x cols [0, b1) per row block) and mirrors it on the host. */
+
+/* Async strided device -> host copy (cudaMemcpy2DAsync): `rows` rows of
+ * `width_bytes` bytes from src (pitch spitch bytes) to dst (pitch dpitch bytes);
+ * dst should be page-locked for the copy to be asynchronous and at full speed. */
+int bgk_memcpy2d_d2h(void *dst, int64_t dpitch, const void *src, int64_t spitch,
+                     int64_t width_bytes, int64_t rows, void *stream);
+
+/* Host mirror of a row block of a symmetric row-major matrix (leading dimension
+ * ld, in doubles): out[j*ld + i] = out[i*ld + j] for i in [r0, r1), j in [0, r0),
+ * i.e. rows [0, r0) x cols [r0, r1) from the lower block, with `nthreads` host
+ * threads (64 x 64 tiles through a thread-local buffer: contiguous reads and
+ * writes).  Host memory only; no CUDA. */
+int bgk_host_mirror_lower(double *out, int64_t ld, int64_t r0, int64_t r1, int nthreads);
+
 /* Test hook for the Matern kernel's branch-free sqrt: fast[i] = the kernel's
  * sqrt_rn_fast(x[i]) where it claims its range (NaN elsewhere), ref[i] =
  * __dsqrt_rn(x[i]).  Device pointers. */

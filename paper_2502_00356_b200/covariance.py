@@ -454,7 +454,9 @@ def generate_covariance(locs, theta: MaternParams, cfg: QuadratureConfig = DEFAU
     host = out if out is not None else np.empty((nrows, N), dtype=np.float64)
     if host.shape != (nrows, N) or host.dtype != np.float64 or not host.flags.c_contiguous:
         raise DomainError(f"out must be a C-contiguous ({nrows}, {N}) float64 array")
-    if nrows and N:
+    if nrows == N and N >= _MIRROR_MIN_N and _is_pinned(host):
+        _full_host_lower_mirrored(plan, lx, ly, N, host, host_block_bytes)
+    elif nrows and N:
         block = max(64, min(nrows, (host_block_bytes // (8 * N)) // 64 * 64))
         host_t = torch.from_numpy(host)
         comp = torch.cuda.current_stream(lx.device)
@@ -478,6 +480,88 @@ def generate_covariance(locs, theta: MaternParams, cfg: QuadratureConfig = DEFAU
         copy.synchronize()
     return CovarianceMatrix(N=N, data=host, tile_size=tile_size, row_begin=r0, row_end=r1,
                             params=theta)
+
+
+_MIRROR_MIN_N = 4096
+_MIRROR_POOL = None
+
+
+def _is_pinned(a: np.ndarray) -> bool:
+    """True when ``a`` is page-locked memory CUDA can copy into asynchronously."""
+    torch = _torch()
+    try:
+        return bool(torch.from_numpy(a).is_pinned())
+    except (RuntimeError, TypeError, ValueError):
+        return False
+
+
+def _host_threads() -> int:
+    import os
+
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def host_d2h_bytes(N: int, rows=None, pinned: bool = True, host_block_bytes: int = 1 << 30) -> int:
+    """Device-to-host bytes generate_covariance moves for a host-array result."""
+    r0, r1 = rows if rows is not None else (0, N)
+    if not (r0 == 0 and r1 == N and N >= _MIRROR_MIN_N and pinned):
+        return 8 * (r1 - r0) * N
+    block = max(64, min(N, (host_block_bytes // (8 * N)) // 64 * 64))
+    return sum(8 * (min(N, b0 + block) - b0) * min(N, b0 + block) for b0 in range(0, N, block))
+
+
+def _full_host_lower_mirrored(plan, lx, ly, N, host, block_bytes):
+    """The whole N x N matrix into a page-locked host array with half the PCIe
+    traffic: per row block [b0, b1) the device computes the lower part
+    cols [0, b1) (bitwise the entries of the full rows), a 2D copy moves just that
+    part, and host threads mirror rows [b0, b1) x cols [0, b0) into
+    rows [0, b0) x cols [b0, b1) while the next block computes and copies.  The
+    mirror of block k writes only rows < b0, which no later copy touches."""
+    global _MIRROR_POOL
+    torch = _torch()
+    L = _lib.lib()
+    if _MIRROR_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _MIRROR_POOL = ThreadPoolExecutor(max_workers=1)  # mirrors in block order
+    nthreads = _host_threads()
+    block = max(64, min(N, (block_bytes // (8 * N)) // 64 * 64))
+    dev = lx.device
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    bufs = [torch.empty((block, N), dtype=torch.float64, device=dev) for _ in range(2)]
+    copied = [None, None]
+    futs = []
+    hp = host.ctypes.data
+
+    def mirror(ev, b0, b1):
+        ev.synchronize()
+        _lib.check(L.bgk_host_mirror_lower(hp, N, b0, b1, nthreads), "bgk_host_mirror_lower")
+
+    try:
+        for bi, b0 in enumerate(range(0, N, block)):
+            b1 = min(N, b0 + block)
+            s = bi % 2
+            if copied[s] is not None:
+                comp.wait_event(copied[s])
+            _tile_launch(plan, lx[b0:b1], ly[b0:b1], lx[:b1], ly[:b1], bufs[s], N,
+                         _lib.LAYOUT_ROW_MAJOR)
+            done = torch.cuda.Event()
+            done.record(comp)
+            copy.wait_event(done)
+            _lib.check(L.bgk_memcpy2d_d2h(hp + 8 * b0 * N, 8 * N, bufs[s].data_ptr(), 8 * N,
+                                          8 * b1, b1 - b0, copy.cuda_stream), "bgk_memcpy2d_d2h")
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            copied[s] = ev
+            futs.append(_MIRROR_POOL.submit(mirror, ev, b0, b1))
+        copy.synchronize()
+    finally:
+        for f in futs:
+            f.result()
 
 
 # ---------------------------------------------------------------------------------------

@@ -4,12 +4,16 @@
 // Matern plan (node tables + Temme constants + u-bucket LUT, i.e. the restated
 // caller of kernels.matern_tile, kernels.py:343-345 / SPEC.md:306-332) and
 // the task-grid arithmetic of the three Matern layouts.
+#include <algorithm>
+#include <emmintrin.h>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -605,3 +609,66 @@ int bgk_enable_peer_access(int peer_device) {
 }
 
 }  // extern "C"
+
+int bgk_memcpy2d_d2h(void *dst, int64_t dpitch, const void *src, int64_t spitch,
+                     int64_t width_bytes, int64_t rows, void *stream) {
+  if (rows < 0 || width_bytes < 0 || width_bytes > dpitch || width_bytes > spitch ||
+      (rows > 0 && width_bytes > 0 && (!dst || !src))) {
+    bgk_set_error("bgk_memcpy2d_d2h: bad arguments");
+    return BGK_ERR_INVALID;
+  }
+  if (rows == 0 || width_bytes == 0) return BGK_OK;
+  const cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch,
+                                          (size_t)width_bytes, (size_t)rows,
+                                          cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    bgk_set_error("cudaMemcpy2DAsync: %s", cudaGetErrorString(e));
+    return BGK_ERR_CUDA;
+  }
+  return BGK_OK;
+}
+
+int bgk_host_mirror_lower(double *out, int64_t ld, int64_t r0, int64_t r1, int nthreads) {
+  if (r0 < 0 || r1 < r0 || ld < r1 || (r1 > r0 && r0 > 0 && !out)) {
+    bgk_set_error("bgk_host_mirror_lower: bad arguments");
+    return BGK_ERR_INVALID;
+  }
+  if (r1 == r0 || r0 == 0) return BGK_OK;
+  constexpr int64_t B = 64;
+  const int64_t nq = (r0 + B - 1) / B;  // destination row tiles (source column tiles)
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads < 1 ? 1 : nthreads, nq));
+  auto work = [&](int t) {
+    alignas(64) double tile[B][B];
+    // static interleave over destination row tiles: disjoint writes per thread
+    for (int64_t qt = t; qt < nq; qt += nt) {
+      const int64_t j0 = qt * B, nj = std::min(B, r0 - j0);
+      for (int64_t i0 = r0; i0 < r1; i0 += B) {
+        const int64_t ni = std::min(B, r1 - i0);
+        for (int64_t i = 0; i < ni; ++i)
+          std::memcpy(tile[i], out + (i0 + i) * ld + j0, (size_t)nj * sizeof(double));
+        for (int64_t j = 0; j < nj; ++j) {
+          double *dst = out + (j0 + j) * ld + i0;
+          if (ni == B && ((uintptr_t)dst & 15) == 0) {
+            // non-temporal stores: the destination lines are written whole, so
+            // skip the read-for-ownership (a third of the mirror's DRAM traffic)
+            for (int64_t i = 0; i < B; i += 2)
+              _mm_stream_pd(dst + i, _mm_set_pd(tile[i + 1][j], tile[i][j]));
+          } else {
+            for (int64_t i = 0; i < ni; ++i) dst[i] = tile[i][j];
+          }
+        }
+      }
+    }
+    _mm_sfence();
+  };
+  if (nt == 1) {
+    work(0);
+    return BGK_OK;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(nt - 1);
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto &th : pool) th.join();
+  return BGK_OK;
+}

@@ -124,6 +124,25 @@ def test_host_output_blocks_bitwise(bg):
     assert np.array_equal(pinned, dev)
 
 
+@pytest.mark.parametrize("N,blk", [(4096, 64), (5003, 640), (4500, 1 << 30)])
+def test_host_lower_mirrored_path_bitwise(bg, N, blk):
+    # page-locked full-matrix output: only the lower triangle crosses PCIe and the
+    # host mirrors it (covariance._full_host_lower_mirrored); must equal the device
+    # matrix bit for bit, whatever the block size
+    from paper_2502_00356_b200 import covariance as C
+
+    assert N >= C._MIRROR_MIN_N
+    rng = np.random.default_rng(N)
+    locs = rng.random((N, 2))
+    locs[7] = locs[3]  # a duplicate location off the diagonal
+    theta = bg.MaternParams(1.0, 0.1, 1.5)
+    dev = bg.generate_covariance(locs, theta, device="cuda").to_numpy()
+    pinned = bg.empty_host_matrix(N, N)
+    pinned.fill(np.nan)
+    bg.generate_covariance(locs, theta, out=pinned, host_block_bytes=blk * 8 * N)
+    assert np.array_equal(pinned, dev)
+
+
 @pytest.mark.parametrize("ts", [1, 7, 64, 100, 256])
 def test_lower_tiles_layout_bitwise(bg, ts):
     rng = np.random.default_rng(13)
