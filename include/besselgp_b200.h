@@ -267,6 +267,11 @@ int bgk_memcpy2d_d2h(void *dst, int64_t dpitch, const void *src, int64_t spitch,
  * writes).  Host memory only; no CUDA. */
 int bgk_host_mirror_lower(double *out, int64_t ld, int64_t r0, int64_t r1, int nthreads);
 
+/* Host memcpy with `nthreads` threads and non-temporal stores (no read-for-ownership
+ * of the destination): the pageable -> page-locked staging copy of host-array
+ * BesselK batches.  Host memory only; no CUDA. */
+int bgk_host_copy(void *dst, const void *src, int64_t bytes, int nthreads);
+
 /* Test hook for the Matern kernel's branch-free sqrt: fast[i] = the kernel's
  * sqrt_rn_fast(x[i]) where it claims its range (NaN elsewhere), ref[i] =
  * __dsqrt_rn(x[i]).  Device pointers. */

@@ -220,8 +220,7 @@ _HOST_CHUNK = 1 << 22  # elements per pipelined chunk for host (numpy) batches
 
 
 _STAGE: dict = {}  # per device: two pinned staging slots (x, nu) of _HOST_CHUNK elements
-_POOL = None       # host threads for the pageable -> pinned copies (numpy releases the GIL)
-_COPY_THREADS = 8
+_COPY_THREADS = None  # host threads of the pageable -> pinned staging copy (default: all)
 
 
 def _stage_slots(torch, dev):
@@ -235,16 +234,20 @@ def _stage_slots(torch, dev):
 
 
 def _par_copy(dst: np.ndarray, src: np.ndarray) -> None:
-    """dst[:] = src with several host threads (pageable -> pinned is memcpy-bound)."""
-    global _POOL
-    if _POOL is None:
-        from concurrent.futures import ThreadPoolExecutor
-        _POOL = ThreadPoolExecutor(max_workers=_COPY_THREADS)
-    n = src.size
-    step = max(1 << 16, -(-n // _COPY_THREADS))
-    futs = [_POOL.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
-    for f in futs:
-        f.result()
+    """dst[:] = src with all host threads and non-temporal stores (bgk_host_copy):
+    the staging copy is host-memory bound and paces the pipeline."""
+    global _COPY_THREADS
+    if _COPY_THREADS is None:
+        import os
+
+        try:
+            _COPY_THREADS = max(1, len(os.sched_getaffinity(0)))
+        except AttributeError:
+            _COPY_THREADS = max(1, os.cpu_count() or 1)
+    assert dst.dtype == src.dtype and dst.size == src.size and dst.flags.c_contiguous \
+        and src.flags.c_contiguous
+    _lib.check(_lib.load_library().bgk_host_copy(dst.ctypes.data, src.ctypes.data, src.nbytes,
+                                                 _COPY_THREADS), "bgk_host_copy")
 
 
 def _bessel_k_host_pipelined(xa, na, cfg, route, validate):

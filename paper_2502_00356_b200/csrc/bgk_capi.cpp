@@ -672,3 +672,47 @@ int bgk_host_mirror_lower(double *out, int64_t ld, int64_t r0, int64_t r1, int n
   for (auto &th : pool) th.join();
   return BGK_OK;
 }
+
+int bgk_host_copy(void *dst, const void *src, int64_t bytes, int nthreads) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) {
+    bgk_set_error("bgk_host_copy: bad arguments");
+    return BGK_ERR_INVALID;
+  }
+  if (bytes == 0) return BGK_OK;
+  char *d = static_cast<char *>(dst);
+  const char *s = static_cast<const char *>(src);
+  // per-thread ranges of whole 4 KB pages; each range streams 16-byte NT stores
+  // once the destination is 16-byte aligned
+  const int64_t page = 4096;
+  const int64_t pages = (bytes + page - 1) / page;
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads < 1 ? 1 : nthreads,
+                                                             pages / 16 + 1));
+  auto work = [&](int t) {
+    const int64_t a = std::min(bytes, (pages * t / nt) * page);
+    const int64_t b = std::min(bytes, (pages * (t + 1) / nt) * page);
+    int64_t i = a;
+    while (i < b && ((uintptr_t)(d + i) & 15)) { d[i] = s[i]; ++i; }
+    for (; i + 64 <= b; i += 64) {
+      const __m128i v0 = _mm_loadu_si128((const __m128i *)(s + i));
+      const __m128i v1 = _mm_loadu_si128((const __m128i *)(s + i + 16));
+      const __m128i v2 = _mm_loadu_si128((const __m128i *)(s + i + 32));
+      const __m128i v3 = _mm_loadu_si128((const __m128i *)(s + i + 48));
+      _mm_stream_si128((__m128i *)(d + i), v0);
+      _mm_stream_si128((__m128i *)(d + i + 16), v1);
+      _mm_stream_si128((__m128i *)(d + i + 32), v2);
+      _mm_stream_si128((__m128i *)(d + i + 48), v3);
+    }
+    for (; i < b; ++i) d[i] = s[i];
+    _mm_sfence();
+  };
+  if (nt == 1) {
+    work(0);
+    return BGK_OK;
+  }
+  std::vector<std::thread> pool;
+  pool.reserve(nt - 1);
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+  work(0);
+  for (auto &th : pool) th.join();
+  return BGK_OK;
+}
