@@ -1,0 +1,102 @@
+"""Parity at BASELINE.json's full sizes (GPU): the M100 matrix (N=100K, 80 GB on the
+device), the 64 Mi-element BesselK batch and shards of the N=200K packed lower-tile
+layout.  The oracle cannot redo them whole, so each check is either a sample the
+oracle recomputes (whole rows, whole tiles, a 1 Mi subsample) or a size-independent
+property of the full result (exact symmetry, exact sigma^2 diagonal, batch-
+composition independence)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SEED = 20250201
+TOL = 1e-10
+
+
+def _rel(a, b):
+    return np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
+
+
+def test_m100_full_matrix(oracle):
+    import paper_2502_00356_b200 as bg
+
+    N = 100_000
+    locs = np.random.default_rng(SEED).random((N, 2))
+    theta = bg.MaternParams(1.0, 0.1, 1.5)
+    out = bg.generate_covariance(locs, theta, device="cuda").data
+    assert out.shape == (N, N)
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([[0, 1, 63, 64, 65, N // 2 - 1, N // 2, N - 33, N - 32, N - 1],
+                                     rng.integers(0, N, 22)]))
+    # whole sampled rows vs the oracle (every column: all buckets, series, tile edges)
+    got = out[torch.from_numpy(rows).cuda()].cpu().numpy()
+    ref = oracle.matern_entries(locs[rows, 0], locs[rows, 1], locs[:, 0], locs[:, 1], 1.0, 0.1, 1.5)
+    err = _rel(got, ref)
+    assert err.max() <= TOL, err.max()
+    # the same rows as columns: exact symmetry across the whole matrix
+    cols = out[:, torch.from_numpy(rows).cuda()].T.cpu().numpy()
+    assert np.array_equal(cols, got)
+    # exact sigma^2 diagonal
+    assert bool((torch.diagonal(out) == 1.0).all())
+    # exact symmetry of random 64 x 64 tile pairs, incl. the partial last tile
+    T = -(-N // 64)
+    for _ in range(300):
+        p, q = sorted(rng.integers(0, T, 2))
+        a = out[64 * p:64 * (p + 1), 64 * q:64 * (q + 1)]
+        b = out[64 * q:64 * (q + 1), 64 * p:64 * (p + 1)]
+        assert torch.equal(a, b.T)
+    del out
+    torch.cuda.empty_cache()
+
+
+def test_bk_full_batch(oracle):
+    import paper_2502_00356_b200 as bg
+
+    n = 64 << 20
+    rng = np.random.default_rng(SEED)
+    x = 140.0 * (1.0 - rng.random(n))
+    nu = 20.0 * (1.0 - rng.random(n))
+    xd, nd = torch.from_numpy(x).cuda(), torch.from_numpy(nu).cuda()
+    full = bg.bessel_k_batch(xd, nd).log_value
+    idx = np.sort(np.random.default_rng(2).choice(n, 1 << 20, replace=False))
+    sub = full[torch.from_numpy(idx).cuda()].cpu().numpy()
+    ref = oracle.refined_log_bessel_batch(x[idx], nu[idx])
+    d = np.abs(sub - ref)
+    assert d.max() <= TOL, d.max()
+    # batch-composition independence: the subsample as its own batch, bit for bit
+    alone = bg.bessel_k_batch(xd[torch.from_numpy(idx).cuda()], nd[torch.from_numpy(idx).cuda()])
+    assert torch.equal(alone.log_value.cpu(), torch.from_numpy(sub))
+
+
+def test_m200_lower_tile_shards(oracle):
+    import paper_2502_00356_b200 as bg
+
+    N, ts = 200_000, 256
+    locs = np.random.default_rng(SEED).random((N, 2))
+    theta = bg.MaternParams(1.0, 0.1, 1.5)
+    T = -(-N // ts)
+    total = T * (T + 1) // 2
+    assert bg.lower_tile_count(N, ts) == total == 306_153
+    for l0, l1 in ((0, 300), (total - 300, total)):
+        cm = bg.generate_covariance(locs, theta, tile_size=ts, layout="lower_tiles",
+                                    tiles=(l0, l1), device="cuda")
+        data = cm.data
+        for l in (l0, l0 + 1, (l0 + l1) // 2, l1 - 2, l1 - 1):
+            p = int((np.sqrt(8.0 * l + 1.0) - 1.0) // 2)
+            while (p + 1) * (p + 2) // 2 <= l:
+                p += 1
+            q = l - p * (p + 1) // 2
+            r = np.arange(p * ts, min(N, (p + 1) * ts))
+            c = np.arange(q * ts, min(N, (q + 1) * ts))
+            tile = data[l - l0].cpu().numpy()  # column-major inside the tile: tile[j, i]
+            got = tile[:len(c), :len(r)].T
+            ref = oracle.matern_entries(locs[r, 0], locs[r, 1], locs[c, 0], locs[c, 1], 1.0, 0.1, 1.5)
+            assert _rel(got, ref).max() <= TOL
+            if p == q:
+                assert np.array_equal(got, got.T)
+            # edge tiles: entries beyond N are zero padding
+            assert not tile[len(c):, :].any() and not tile[:, len(r):].any()
+        del data, cm
+        torch.cuda.empty_cache()
