@@ -67,7 +67,10 @@ constexpr int kNuStep = BGK_BK_NUSTEP;
 constexpr int kNuCells = 24 * kNuStep;            // nu cells of width 1/kNuStep, last open-ended
 constexpr int kXKeyBase = (1023 - 6) << kXBits;
 constexpr int kMaxPred = 63;  // predicted window size (sort key), clamped
-constexpr int kBuckets = kMaxPred + 2;  // + series bucket
+// buckets: 0 series | 2 pb - 1 + (anchor not 0), pb = 1 (widest) .. kMaxPred - 1 |
+// kBuckets - 1 reference path.  Elements whose anchor is node 0 (a^2 <= x) sort
+// next to each other so whole warps skip the two anchor-shift exps.
+constexpr int kBuckets = 2 * kMaxPred + 2;
 
 struct BkArgs {
   const double *x;
@@ -154,9 +157,15 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
   const double tlo = A.t0 + (double)lo * A.h;
   double E, Ei;
   exp_pair(a * A.h, t128, E, Ei);
-  double P = exp_acc(-a * (ta - tlo), t128);  // E^{lo - m}
-  const double qa = a * (ta + tlo);
-  double Qs = (qa < 700.0) ? exp_acc(-qa, t128) : 0.0;  // q E^{m - lo}
+  // E^{lo - m} and q E^{m - lo}.  With the anchor at node 0 of a grid starting at
+  // t0 = 0 both are exactly 1 (lo = m = 0: exp of +-0); warps whose lanes all have
+  // m = 0 (sorted together by the classify pass) skip the two exps.
+  double P = 1.0, Qs = 1.0;
+  if (!(A.t0 == 0.0 && __all_sync(0xffffffffu, m == 0))) {
+    P = exp_acc(-a * (ta - tlo), t128);
+    const double qa = a * (ta + tlo);
+    Qs = (qa < 700.0) ? exp_acc(-qa, t128) : 0.0;
+  }
   const double mx = -x, xca = x * ca;
   const double2 *row = cw + lo;
   double acc = 0.0;
@@ -249,7 +258,7 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
       }
       if (w) {
         const int nw = (int)(w & 0xffff) + (int)(w >> 16) + 1;
-        b = kMaxPred - min(nw, kMaxPred - 1);
+        b = 2 * (kMaxPred - min(nw, kMaxPred - 1)) - (a * a <= x ? 1 : 0);
       }
     }
     sw[e] = w;
@@ -257,10 +266,11 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
     atomicAdd(&hist[b], 1);
   }
   __syncthreads();
-  if (tid < 32) {  // exclusive scan over kBuckets (<= 65) bins, 3 per lane
-    int v[3], local = 0;
-    for (int t = 0; t < 3; ++t) {
-      const int b = lane * 3 + t;
+  static_assert(kBuckets <= 128, "scan: 4 buckets per lane");
+  if (tid < 32) {  // exclusive scan over kBuckets (<= 128) bins, 4 per lane
+    int v[4], local = 0;
+    for (int t = 0; t < 4; ++t) {
+      const int b = lane * 4 + t;
       v[t] = b < kBuckets ? hist[b] : 0;
       local += v[t];
     }
@@ -270,8 +280,8 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
       if (lane >= o) incl += w;
     }
     int run = incl - local;
-    for (int t = 0; t < 3; ++t) {
-      const int b = lane * 3 + t;
+    for (int t = 0; t < 4; ++t) {
+      const int b = lane * 4 + t;
       if (b < kBuckets) hist[b] = run;
       run += v[t];
     }
