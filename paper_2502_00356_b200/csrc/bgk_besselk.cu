@@ -86,6 +86,7 @@ struct BkArgs {
   int table_ok;  // 1: c table fits in shared memory and t0 >= 0 -> fast path allowed
   const uint32_t *win;  // device: per (x, nu) cell, U | D << 16 (window above / below anchor)
   const double2 *cwg;   // device: {cosh t_k, weight exponent adjust}, k = 0..bins (host libm cosh)
+  float t0f, hinvf, binsf;  // anchor_node_fast's fp32 constants
 };
 
 __host__ __device__ inline int x_cell(double x) {
@@ -118,13 +119,22 @@ __host__ __device__ inline int anchor_node(double x, double a, double t0, double
 // window then shifts by one node (dropping an edge term of relative size
 // <~ e^-30 on 1e-5 of elements at worst), and the anchor itself only
 // sets the scale of the sum (rounding-level effect).
-__device__ __forceinline__ int anchor_node_fast(double x, double a, double t0, double h, int bins) {
+// (t0f = (float)t0, hinvf = (float)(1.0 / h), binsf = (float)bins: precomputed on
+// the host, read from the parameter bank -- no live registers / spills)
+__device__ __forceinline__ int anchor_node_fast(double x, double a, float t0f, float hinvf,
+                                                float binsf) {
   if (a * a <= x) return 0;
   const float z = __fdividef((float)a, (float)x);
   const float ts = __logf(z + sqrtf(fmaf(z, z, 1.0f)));
-  float fm = rintf((ts - (float)t0) * (float)(1.0 / h));
-  fm = fminf(fmaxf(fm, 0.0f), (float)bins);
+  float fm = rintf((ts - t0f) * hinvf);
+  fm = fminf(fmaxf(fm, 0.0f), binsf);
   return (int)fm;
+}
+
+__device__ __forceinline__ int ld_u16_volatile(const uint16_t *p) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
 }
 
 __device__ __forceinline__ bool in_table(double x, double a) {
@@ -147,7 +157,7 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
                                                     const double *__restrict__ invc,
                                                     const double *__restrict__ logc) {
   const int bins = A.bins;
-  const int m = active ? anchor_node_fast(x, a, A.t0, A.h, bins) : 0;
+  const int m = active ? anchor_node_fast(x, a, A.t0f, A.hinvf, A.binsf) : 0;
   const int U = min((int)(w & 0xffff), bins - m), D = min((int)(w >> 16), m);
   const int lo = m - D, n = active ? U + D + 1 : 0;
   const int nmax = __reduce_max_sync(0xffffffffu, n);
@@ -205,6 +215,7 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
   __shared__ double s_exp[128], s_invc[128], s_logc[128];
   __shared__ int hist[kBuckets + 1];
   __shared__ int s_next;
+  __shared__ uint16_t s_eidx[kBkThreads];
   // dynamic: the chunk at fixed offsets (no pointer registers), then
   // {cosh t_k, ln w_k} (bins + 1, only when table_ok)
   const int ncw = A.table_ok ? A.bins + 1 : 0;
@@ -311,7 +322,9 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
     if (g >= ngroups) break;
     const int p = g * 32 + lane;
     const bool valid = p < cnt;
-    const int e = valid ? perm[p] : 0;
+    const int e0 = valid ? perm[p] : 0;
+    s_eidx[tid] = (uint16_t)e0;  // re-read for the result stores (not spilled)
+    const int e = e0;
     const double x = valid ? sx[e] : 1.0, nu = valid ? snu[e] : 0.0;
     const uint32_t w = valid ? sw[e] : 0u;
     const bool series = (A.route == 1) || (A.route == 0 && x < A.thr);
@@ -325,9 +338,10 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
     } else if (!fast) {
       lk = fixed_window_log_ref(x, nu, A.t0, A.t1, A.bins);
     }
-    sx[e] = lk;
-    if (A.k) snu[e] = (fabs(lk) < 700.0) ? exp_acc(lk, s_exp) : exp(lk);
-    spath[e] = series ? 0 : 1;
+    const int er = ld_u16_volatile(&s_eidx[tid]);
+    sx[er] = lk;
+    if (A.k) snu[er] = (fabs(lk) < 700.0) ? exp_acc(lk, s_exp) : exp(lk);
+    spath[er] = series ? 0 : 1;
   }
   __syncthreads();
   // coalesced streaming stores, fixed trip count (all of a thread's stores in flight)
@@ -491,6 +505,9 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
   A.cap = cfg->series_cap;
   A.bins = (int)cfg->bins;
   A.route = route;
+  A.t0f = (float)A.t0;
+  A.hinvf = (float)(1.0 / A.h);
+  A.binsf = (float)A.bins;
   const int64_t kMaxTable = 8191;  // 128 KB of shared memory ({c, ln w} pairs)
   A.table_ok = (cfg->t_lower >= 0.0 && cfg->bins <= kMaxTable) ? 1 : 0;
   A.win = nullptr;
