@@ -210,6 +210,13 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
   return (a * ta - kLn2) - xca + log_fast(A.h * acc, invc, logc);
 }
 
+// The Temme path (x < threshold: 0.08% of the BK elements) out of line, so its
+// long chain does not take registers from the fast path's loop.
+__device__ __noinline__ double bk_series_log(double x, double nu, double eps, long long cap) {
+  const TemmeConst T = temme_const(nu);
+  return temme_series_log_c(x, T, eps, cap);
+}
+
 __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_constant__ BkArgs A) {
   extern __shared__ __align__(16) unsigned char bk_smem[];
   __shared__ double s_exp[128], s_invc[128], s_logc[128];
@@ -333,8 +340,7 @@ __global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_con
     double lk = fixed_window_fast(fast, x, a, w, A, cw, s_exp, s_invc, s_logc);
     if (!valid) continue;
     if (series) {
-      const TemmeConst T = temme_const(nu);
-      lk = temme_series_log_c(x, T, A.eps, A.cap);
+      lk = bk_series_log(x, nu, A.eps, A.cap);
     } else if (!fast) {
       lk = fixed_window_log_ref(x, nu, A.t0, A.t1, A.bins);
     }
