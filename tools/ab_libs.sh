@@ -7,6 +7,7 @@ LIB=paper_2502_00356_b200/libbesselgp_sm100a.so
 cp $LIB /tmp/lib_orig.so
 WL="--no-secondary"
 if [ "$1" == "--bk" ]; then WL="--workload bk"; shift; fi
+if [ "$1" == "--wl" ]; then WL="--workload $2 --no-secondary"; shift 2; fi
 for rep in 1 2; do
   for V in "$@"; do
     cp "$V" $LIB
