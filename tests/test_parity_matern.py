@@ -296,3 +296,23 @@ def test_pow_mode_matches_general_power(bg, oracle, nu):
     assert np.max(rel_err(fast, gen)) <= 1e-13
     ref = oracle.generate_covariance(locs, 1.7, 0.1, nu)
     assert np.max(rel_err(fast, ref)) <= TOL
+
+
+def test_concurrent_streams_bitwise(bg):
+    # re-entrancy: launches on two streams at once (persistent kernels with task
+    # counters per stream) give the same matrices as one after the other
+    import torch
+
+    rng = np.random.default_rng(33)
+    locs_a, locs_b = rng.random((3000, 2)), rng.random((2500, 2))
+    th_a, th_b = bg.MaternParams(1.0, 0.1, 1.5), bg.MaternParams(2.0, 0.05, 0.8)
+    ref_a = bg.generate_covariance(locs_a, th_a, device="cuda").data.clone()
+    ref_b = bg.generate_covariance(locs_b, th_b, device="cuda").data.clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        a = bg.generate_covariance(locs_a, th_a, device="cuda").data
+    with torch.cuda.stream(s2):
+        b = bg.generate_covariance(locs_b, th_b, device="cuda").data
+    torch.cuda.synchronize()
+    assert torch.equal(a, ref_a) and torch.equal(b, ref_b)
