@@ -47,8 +47,17 @@
 
 namespace bgk {
 
-constexpr int kBkThreads = 256;
-constexpr int kBkPerThread = 8;
+#ifndef BGK_BK_THREADS
+#define BGK_BK_THREADS 256  // A/B on B200: 128 threads x 8 (7 CTAs/SM) 1.68 ms, 128 x 16 2.00 ms, 256 x 8 1.54 ms
+#endif
+#ifndef BGK_BK_PER_THREAD
+#define BGK_BK_PER_THREAD 8
+#endif
+#ifndef BGK_BK_MINBLOCKS
+#define BGK_BK_MINBLOCKS 4
+#endif
+constexpr int kBkThreads = BGK_BK_THREADS;
+constexpr int kBkPerThread = BGK_BK_PER_THREAD;
 constexpr int kBkChunk = kBkThreads * kBkPerThread;
 constexpr int kBkChunkBytes = kBkChunk * (8 + 8 + 4 + 2 + 1 + 1);  // + 1: keeps cw 16-B aligned
 #ifndef BGK_BK_XBITS
@@ -217,7 +226,7 @@ __device__ __noinline__ double bk_series_log(double x, double nu, double eps, lo
   return temme_series_log_c(x, T, eps, cap);
 }
 
-__global__ void __launch_bounds__(kBkThreads, 4) besselk_kernel(const __grid_constant__ BkArgs A) {
+__global__ void __launch_bounds__(kBkThreads, BGK_BK_MINBLOCKS) besselk_kernel(const __grid_constant__ BkArgs A) {
   extern __shared__ __align__(16) unsigned char bk_smem[];
   __shared__ double s_exp[128], s_invc[128], s_logc[128];
   __shared__ int hist[kBuckets + 1];
