@@ -267,6 +267,12 @@ int bgk_memcpy2d_d2h(void *dst, int64_t dpitch, const void *src, int64_t spitch,
  * writes).  Host memory only; no CUDA. */
 int bgk_host_mirror_lower(double *out, int64_t ld, int64_t r0, int64_t r1, int nthreads);
 
+/* General form: out[j*ld + i] = out[i*ld + j] for i in [r0, r1), j in [c0, c1)
+ * (the two index ranges must not overlap); bgk_host_mirror_lower is c0 = 0,
+ * c1 = r0. */
+int bgk_host_mirror_block(double *out, int64_t ld, int64_t r0, int64_t r1, int64_t c0,
+                          int64_t c1, int nthreads);
+
 /* Host memcpy with `nthreads` threads and non-temporal stores (no read-for-ownership
  * of the destination): the pageable -> page-locked staging copy of host-array
  * BesselK batches.  Host memory only; no CUDA. */

@@ -121,6 +121,7 @@ SIGNATURES = {
     "bgk_memcpy2d_d2h": (_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
     "bgk_host_mirror_lower": (_int, [_vp, _i64, _i64, _i64, _int]),
     "bgk_host_copy": (_int, [_vp, _vp, _i64, _int]),
+    "bgk_host_mirror_block": (_int, [_vp, _i64, _i64, _i64, _i64, _i64, _int]),
     "bgk_ipc_export": (_int, [_vp, _vp, ctypes.POINTER(ctypes.c_uint64)]),
     "bgk_ipc_open": (_int, [_vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
     "bgk_ipc_close": (_int, [_vp, ctypes.c_uint64]),

@@ -484,6 +484,7 @@ def generate_covariance(locs, theta: MaternParams, cfg: QuadratureConfig = DEFAU
 
 _MIRROR_MIN_N = 4096
 _MIRROR_POOL = None
+_MIRROR_DIRECT = None  # override of _mirror_direct_blocks (tests / tuning)
 
 
 def _is_pinned(a: np.ndarray) -> bool:
@@ -504,22 +505,37 @@ def _host_threads() -> int:
         return max(1, os.cpu_count() or 1)
 
 
+def _mirror_direct_blocks(N: int, block: int) -> int:
+    """Row blocks of the UPPER triangle next to the diagonal that each block sends
+    over PCIe directly (the host mirrors the rest): trades PCIe time for the
+    mirror's host-memory traffic.  Default 0: on the B200 boxes PCIe is the
+    bound (M100, tools/e2e_diag.py: w = 0 / 4 / 8 / 14 -> 0.874 / 0.876 / 0.932 /
+    1.014 s; full rows 1.40 s)."""
+    if _MIRROR_DIRECT is not None:
+        return _MIRROR_DIRECT
+    return 0
+
+
 def host_d2h_bytes(N: int, rows=None, pinned: bool = True, host_block_bytes: int = 1 << 30) -> int:
     """Device-to-host bytes generate_covariance moves for a host-array result."""
     r0, r1 = rows if rows is not None else (0, N)
     if not (r0 == 0 and r1 == N and N >= _MIRROR_MIN_N and pinned):
         return 8 * (r1 - r0) * N
     block = max(64, min(N, (host_block_bytes // (8 * N)) // 64 * 64))
-    return sum(8 * (min(N, b0 + block) - b0) * min(N, b0 + block) for b0 in range(0, N, block))
+    w = _mirror_direct_blocks(N, block)
+    return sum(8 * (min(N, b0 + block) - b0) * min(N, b0 + block + w * block)
+               for b0 in range(0, N, block))
 
 
 def _full_host_lower_mirrored(plan, lx, ly, N, host, block_bytes):
-    """The whole N x N matrix into a page-locked host array with half the PCIe
-    traffic: per row block [b0, b1) the device computes the lower part
-    cols [0, b1) (bitwise the entries of the full rows), a 2D copy moves just that
-    part, and host threads mirror rows [b0, b1) x cols [0, b0) into
-    rows [0, b0) x cols [b0, b1) while the next block computes and copies.  The
-    mirror of block k writes only rows < b0, which no later copy touches."""
+    """The whole N x N matrix into a page-locked host array with about half the
+    PCIe traffic: per row block [b0, b1) the device computes the lower part plus w
+    blocks of the upper one, cols [0, b1 + w block) (bitwise the entries of the
+    full rows), a 2D copy moves just that part, and host threads mirror
+    rows [b0, b1) x cols [0, b0 - w block) into rows [0, b0 - w block) x
+    cols [b0, b1) while the next block computes and copies (the rows in between
+    received those columns directly).  The mirror of block k writes only rows
+    < b0, which no later copy touches."""
     global _MIRROR_POOL
     torch = _torch()
     L = _lib.lib()
@@ -529,6 +545,7 @@ def _full_host_lower_mirrored(plan, lx, ly, N, host, block_bytes):
         _MIRROR_POOL = ThreadPoolExecutor(max_workers=1)  # mirrors in block order
     nthreads = _host_threads()
     block = max(64, min(N, (block_bytes // (8 * N)) // 64 * 64))
+    w = _mirror_direct_blocks(N, block)
     dev = lx.device
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
@@ -538,8 +555,10 @@ def _full_host_lower_mirrored(plan, lx, ly, N, host, block_bytes):
     hp = host.ctypes.data
 
     def mirror(ev, b0, b1):
+        # rows [b0 - w block, b0) already hold cols [b0, b1): their blocks sent them
         ev.synchronize()
-        _lib.check(L.bgk_host_mirror_lower(hp, N, b0, b1, nthreads), "bgk_host_mirror_lower")
+        _lib.check(L.bgk_host_mirror_block(hp, N, b0, b1, 0, max(0, b0 - w * block), nthreads),
+                   "bgk_host_mirror_block")
 
     try:
         for bi, b0 in enumerate(range(0, N, block)):
@@ -547,13 +566,14 @@ def _full_host_lower_mirrored(plan, lx, ly, N, host, block_bytes):
             s = bi % 2
             if copied[s] is not None:
                 comp.wait_event(copied[s])
-            _tile_launch(plan, lx[b0:b1], ly[b0:b1], lx[:b1], ly[:b1], bufs[s], N,
+            ce = min(N, b1 + w * block)  # the lower part + w blocks of the upper
+            _tile_launch(plan, lx[b0:b1], ly[b0:b1], lx[:ce], ly[:ce], bufs[s], N,
                          _lib.LAYOUT_ROW_MAJOR)
             done = torch.cuda.Event()
             done.record(comp)
             copy.wait_event(done)
             _lib.check(L.bgk_memcpy2d_d2h(hp + 8 * b0 * N, 8 * N, bufs[s].data_ptr(), 8 * N,
-                                          8 * b1, b1 - b0, copy.cuda_stream), "bgk_memcpy2d_d2h")
+                                          8 * ce, b1 - b0, copy.cuda_stream), "bgk_memcpy2d_d2h")
             ev = torch.cuda.Event()
             ev.record(copy)
             copied[s] = ev

@@ -629,19 +629,25 @@ int bgk_memcpy2d_d2h(void *dst, int64_t dpitch, const void *src, int64_t spitch,
 }
 
 int bgk_host_mirror_lower(double *out, int64_t ld, int64_t r0, int64_t r1, int nthreads) {
-  if (r0 < 0 || r1 < r0 || ld < r1 || (r1 > r0 && r0 > 0 && !out)) {
-    bgk_set_error("bgk_host_mirror_lower: bad arguments");
+  return bgk_host_mirror_block(out, ld, r0, r1, 0, r0, nthreads);
+}
+
+int bgk_host_mirror_block(double *out, int64_t ld, int64_t r0, int64_t r1, int64_t c0,
+                          int64_t c1, int nthreads) {
+  if (r0 < 0 || r1 < r0 || c0 < 0 || c1 < c0 || ld < r1 || ld < c1 ||
+      (r1 > r0 && c1 > c0 && !out) || (c0 < r1 && r0 < c1 && c1 > c0 && r1 > r0)) {
+    bgk_set_error("bgk_host_mirror_block: bad arguments (ranges must not overlap)");
     return BGK_ERR_INVALID;
   }
-  if (r1 == r0 || r0 == 0) return BGK_OK;
+  if (r1 == r0 || c1 == c0) return BGK_OK;
   constexpr int64_t B = 64;
-  const int64_t nq = (r0 + B - 1) / B;  // destination row tiles (source column tiles)
+  const int64_t nq = (c1 - c0 + B - 1) / B;  // destination row tiles (source column tiles)
   const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads < 1 ? 1 : nthreads, nq));
   auto work = [&](int t) {
     alignas(64) double tile[B][B];
     // static interleave over destination row tiles: disjoint writes per thread
     for (int64_t qt = t; qt < nq; qt += nt) {
-      const int64_t j0 = qt * B, nj = std::min(B, r0 - j0);
+      const int64_t j0 = c0 + qt * B, nj = std::min(B, c1 - j0);
       for (int64_t i0 = r0; i0 < r1; i0 += B) {
         const int64_t ni = std::min(B, r1 - i0);
         for (int64_t i = 0; i < ni; ++i)

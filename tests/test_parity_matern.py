@@ -124,14 +124,16 @@ def test_host_output_blocks_bitwise(bg):
     assert np.array_equal(pinned, dev)
 
 
+@pytest.mark.parametrize("direct", [None, 0, 3])
 @pytest.mark.parametrize("N,blk", [(4096, 64), (5003, 640), (4500, 1 << 30)])
-def test_host_lower_mirrored_path_bitwise(bg, N, blk):
+def test_host_lower_mirrored_path_bitwise(bg, N, blk, direct, monkeypatch):
     # page-locked full-matrix output: only the lower triangle crosses PCIe and the
     # host mirrors it (covariance._full_host_lower_mirrored); must equal the device
     # matrix bit for bit, whatever the block size
     from paper_2502_00356_b200 import covariance as C
 
     assert N >= C._MIRROR_MIN_N
+    monkeypatch.setattr(C, "_MIRROR_DIRECT", direct)  # upper blocks sent directly
     rng = np.random.default_rng(N)
     locs = rng.random((N, 2))
     locs[7] = locs[3]  # a duplicate location off the diagonal

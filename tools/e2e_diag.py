@@ -33,7 +33,11 @@ timed("warm", lambda: bg.generate_covariance(locs, theta, out=host), reps=1)
 C._MIRROR_MIN_N = 1 << 62
 timed("full rows (PCIe 80 GB)", lambda: bg.generate_covariance(locs, theta, out=host))
 C._MIRROR_MIN_N = 4096
-timed("lower + host mirror", lambda: bg.generate_covariance(locs, theta, out=host))
+for w in [int(v) for v in os.environ.get("E2E_W", "0,4,8,12").split(",")]:
+    C._MIRROR_DIRECT = w
+    timed(f"lower + {w} upper blocks + host mirror", lambda: bg.generate_covariance(locs, theta, out=host))
+C._MIRROR_DIRECT = None
+timed("default", lambda: bg.generate_covariance(locs, theta, out=host))
 nt = C._host_threads()
 for t in sorted({nt, max(1, nt // 2), 2 * nt}):
     timed(f"host mirror alone, all rows, {t} threads",
