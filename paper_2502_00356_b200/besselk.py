@@ -201,19 +201,27 @@ def bessel_k_batch(x, nu, cfg: QuadratureConfig = DEFAULT_CONFIG, route: str = "
     return BatchResult(logk.cpu().numpy(), k.cpu().numpy(), path.cpu().numpy())
 
 
+def _bad_mask(xd, nud, cfg, route):
+    torch = _torch()
+    bad = ~torch.isfinite(xd) | (xd <= 0.0) | ~torch.isfinite(nud) | (nud < 0.0)
+    if route == "series":
+        bad |= xd >= cfg.small_x_threshold
+    return bad
+
+
+def _raise_for(xv: float, nv: float, cfg, route):
+    EvalPoint(xv, nv)  # raises the reference's message for non-finite / negative
+    if route == "series":
+        raise DomainError(f"series path needs 0 < x < {cfg.small_x_threshold:g}, got {xv!r}")
+    raise DomainError("x must be positive (r = 0 is handled by the Matern kernel)")
+
+
 def _validate_batch(xd, nud, cfg, route):
     torch = _torch()
-    bad_x = ~torch.isfinite(xd) | (xd <= 0.0)
-    bad_nu = ~torch.isfinite(nud) | (nud < 0.0)
-    if route == "series":
-        bad_x |= xd >= cfg.small_x_threshold
-    if bool(bad_x.any()) or bool(bad_nu.any()):
-        i = int(torch.nonzero(bad_x | bad_nu)[0])
-        xv, nv = float(xd[i]), float(nud[i])
-        EvalPoint(xv, nv)  # raises the reference's message for non-finite / negative
-        if route == "series":
-            raise DomainError(f"series path needs 0 < x < {cfg.small_x_threshold:g}, got {xv!r}")
-        raise DomainError("x must be positive (r = 0 is handled by the Matern kernel)")
+    bad = _bad_mask(xd, nud, cfg, route)
+    if bool(bad.any()):
+        i = int(torch.nonzero(bad)[0])
+        _raise_for(float(xd[i]), float(nud[i]), cfg, route)
 
 
 _HOST_CHUNK = 1 << 22  # elements per pipelined chunk for host (numpy) batches
@@ -269,6 +277,7 @@ def _bessel_k_host_pipelined(xa, na, cfg, route, validate):
     inp = torch.cuda.Stream(dev)
     copy = torch.cuda.Stream(dev)
     slots = _stage_slots(torch, dev)
+    bad_any = None  # device flag: some element failed validation
     staged = [None, None]  # event: the slot's H2D has finished (slot reusable)
     freed = [None, None]   # event: the chunk's D2H has finished (device buffers reusable)
     for ci, c0 in enumerate(range(0, n, _HOST_CHUNK)):
@@ -290,8 +299,9 @@ def _bessel_k_host_pipelined(xa, na, cfg, route, validate):
         comp.wait_event(ev_in)
         xd.record_stream(comp)
         nd.record_stream(comp)
-        if validate:
-            _validate_batch(xd, nd, cfg, route)
+        if validate:  # deferred: one device flag for the whole call, no per-chunk sync
+            b = _bad_mask(xd, nd, cfg, route).any()
+            bad_any = b if bad_any is None else bad_any | b
         logk, k, path = _launch_besselk(xd, nd, cfg, _ROUTES[route])
         done = torch.cuda.Event()
         done.record(comp)
@@ -308,6 +318,13 @@ def _bessel_k_host_pipelined(xa, na, cfg, route, validate):
         path.record_stream(copy)
         freed[s] = ev
     copy.synchronize()
+    if bad_any is not None and bool(bad_any):
+        # the first offending element, in order, gets the reference's message
+        bad = ~np.isfinite(xf) | (xf <= 0.0) | ~np.isfinite(nf) | (nf < 0.0)
+        if route == "series":
+            bad |= xf >= cfg.small_x_threshold
+        i = int(np.flatnonzero(bad)[0])
+        _raise_for(float(xf[i]), float(nf[i]), cfg, route)
     return BatchResult(out_l.numpy().reshape(shape), out_k.numpy().reshape(shape),
                        out_p.numpy().reshape(shape))
 

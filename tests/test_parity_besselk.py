@@ -204,3 +204,13 @@ def test_host_pipeline_matches_device_path(bg):
         bad = x.copy()
         bad[n - 5] = -1.0
         bg.bessel_k_batch(bad, nu)
+    # deferred validation reports the FIRST offending element with its own message
+    bad = x.copy()
+    bad[n // 2] = -1.0
+    badnu = nu.copy()
+    badnu[n // 3] = np.nan
+    with pytest.raises(bg.DomainError) as first:
+        bg.bessel_k_batch(bad, badnu)
+    with pytest.raises(bg.DomainError) as single:
+        bg.EvalPoint(float(x[n // 3]), float("nan"))
+    assert str(first.value) == str(single.value)
