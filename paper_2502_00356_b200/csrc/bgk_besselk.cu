@@ -63,6 +63,10 @@ constexpr int kBkChunkBytes = kBkChunk * (8 + 8 + 4 + 2 + 1 + 1);  // + 1: keeps
 #ifndef BGK_BK_XBITS
 #define BGK_BK_XBITS 2  // window table: 2^XBITS x cells per octave
 #endif
+#ifndef BGK_BK_DYN_TAIL
+#define BGK_BK_DYN_TAIL 4  // groups per warp pulled dynamically at the end of the compute phase
+                          // (A/B on B200: 1 -> 1.556, 2 -> 1.534, 4 -> 1.512, 8 -> 1.542 ms)
+#endif
 #ifndef BGK_BK_MARGIN
 #define BGK_BK_MARGIN 0  // nodes added to each side of the sampled window extents (A/B on
                          // B200: 0 -> 1.606 ms, 1 -> 1.661 ms; max|d ln K| unchanged, 5.7e-14)
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(kBkThreads, BGK_BK_MINBLOCKS) besselk_kernel(c
   // nothing) so it runs branch-free.
   const int ngroups = (cnt + 31) >> 5;
   constexpr int kWarps = kBkThreads / 32;
-  const int nstatic = max(0, (ngroups - 2 * kWarps) / kWarps);
+  const int nstatic = max(0, (ngroups - BGK_BK_DYN_TAIL * kWarps) / kWarps);
   const int warp = tid >> 5;
   for (int round = 0;; ++round) {
     int g;
