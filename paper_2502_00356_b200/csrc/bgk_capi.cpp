@@ -98,11 +98,11 @@ Window window_at(const bgk_matern_plan &P, double u) {
 // no safe LUT can be built.
 bool build_lut_at(bgk_matern_plan &P, int shift);
 void build_lut(bgk_matern_plan &P) {
-  // 16 buckets per octave measured best on B200 (the 32-per-octave table's
-  // tighter windows do not pay for its larger histogram); BGK_LUT_KEY_SHIFT=15
-  // selects it for experiments.
+  // 32 buckets per octave (key shift 15) when the table fits, else 16: the tighter
+  // windows now pay for the larger histogram (A/B on B200, v18 kernels: M100
+  // 88.88 vs 89.45 ms, M50 -0.4%); BGK_LUT_KEY_SHIFT=16 forces 16 per octave.
   const char *env = std::getenv("BGK_LUT_KEY_SHIFT");
-  const int first = (env && std::atoi(env) == 15) ? 15 : 16;
+  const int first = (env && std::atoi(env) == 16) ? 16 : 15;
   for (int shift = first; shift <= 16; ++shift)
     if (build_lut_at(P, shift)) return;
 }
