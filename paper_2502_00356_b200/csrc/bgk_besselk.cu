@@ -63,6 +63,10 @@ constexpr int kBkChunkBytes = kBkChunk * (8 + 8 + 4 + 2 + 1 + 1);  // + 1: keeps
 #ifndef BGK_BK_XBITS
 #define BGK_BK_XBITS 2  // window table: 2^XBITS x cells per octave
 #endif
+#ifndef BGK_BK_NODE_UNROLL
+#define BGK_BK_NODE_UNROLL 2
+#endif
+constexpr int kBkNodeUnroll = BGK_BK_NODE_UNROLL;
 #ifndef BGK_BK_DYN_TAIL
 #define BGK_BK_DYN_TAIL 4  // groups per warp pulled dynamically at the end of the compute phase
                           // (A/B on B200: 1 -> 1.556, 2 -> 1.534, 4 -> 1.512, 8 -> 1.542 ms)
@@ -214,7 +218,7 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
     return s * T * p;  // (s T) p: T scaling is exact
   };
   int j = 0;
-#pragma unroll 2
+#pragma unroll(kBkNodeUnroll)
   for (; j < nmin; ++j) acc += node(row[j]);
   for (; j < nmax; ++j) {
     const double t = node(row[min(j, bins - lo)]);
