@@ -100,3 +100,23 @@ def test_m200_lower_tile_shards(oracle):
             assert not tile[len(c):, :].any() and not tile[:, len(r):].any()
         del data, cm
         torch.cuda.empty_cache()
+
+
+def test_m100_host_buffer_path():
+    # the e2e path at full size: the 80 GB matrix into page-locked host memory with
+    # only the lower triangle over PCIe and the upper triangle mirrored on the host
+    import paper_2502_00356_b200 as bg
+
+    N = 100_000
+    locs = np.random.default_rng(SEED).random((N, 2))
+    theta = bg.MaternParams(1.0, 0.1, 1.5)
+    host = bg.empty_host_matrix(N, N)
+    bg.generate_covariance(locs, theta, out=host)
+    rng = np.random.default_rng(3)
+    rows = np.unique(np.concatenate([[0, 1279, 1280, N // 2, N - 1], rng.integers(0, N, 27)]))
+    for r in rows:
+        dev = bg.generate_covariance(locs, theta, rows=(int(r), int(r) + 1), device="cuda").data
+        assert np.array_equal(host[r], dev.cpu().numpy()[0])
+        assert np.array_equal(host[:, r], host[r])  # the mirrored column
+    assert np.array_equal(np.diagonal(host), np.ones(N))
+    del host
