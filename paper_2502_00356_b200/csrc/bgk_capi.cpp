@@ -12,7 +12,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
+#include <pthread.h>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -610,6 +614,84 @@ int bgk_enable_peer_access(int peer_device) {
 
 }  // extern "C"
 
+namespace {
+// A persistent host thread pool for the host-side helpers (staging copies, matrix
+// mirror): they run many times per call (per chunk / per row block), and spawning
+// and joining threads each time costs tens of microseconds per thread.  One job
+// at a time; the calling thread takes part.
+class HostPool {
+ public:
+  template <class F>
+  void run(int n, F &&f) {
+    if (n <= 1) {
+      if (n == 1) f(0);
+      return;
+    }
+    std::lock_guard<std::mutex> one_job(job_mu_);
+    grow(n - 1);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = [&f](int i) { f(i); };
+      njobs_ = n;
+      next_.store(0);
+      remaining_ = n;
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return remaining_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void grow(int want) {
+    while ((int)workers_.size() < want) workers_.emplace_back([this] { loop(); });
+  }
+  void drain() {
+    for (;;) {
+      const int i = next_.fetch_add(1);
+      if (i >= njobs_) return;
+      job_(i);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--remaining_ == 0) done_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      drain();
+    }
+  }
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> workers_;
+  std::function<void(int)> job_;
+  int njobs_ = 0, remaining_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+};
+
+// never destroyed (workers outlive main's statics); a forked child starts with a
+// fresh pool, since the parent's worker threads do not exist there
+HostPool *g_host_pool = nullptr;
+std::once_flag g_host_pool_once;
+
+template <class F>
+void host_parallel_for(int n, F &&f) {
+  std::call_once(g_host_pool_once, [] {
+    g_host_pool = new HostPool();
+    pthread_atfork(nullptr, nullptr, [] { g_host_pool = new HostPool(); });
+  });
+  g_host_pool->run(n, std::forward<F>(f));
+}
+}  // namespace
+
 int bgk_memcpy2d_d2h(void *dst, int64_t dpitch, const void *src, int64_t spitch,
                      int64_t width_bytes, int64_t rows, void *stream) {
   if (rows < 0 || width_bytes < 0 || width_bytes > dpitch || width_bytes > spitch ||
@@ -671,11 +753,7 @@ int bgk_host_mirror_block(double *out, int64_t ld, int64_t r0, int64_t r1, int64
     work(0);
     return BGK_OK;
   }
-  std::vector<std::thread> pool;
-  pool.reserve(nt - 1);
-  for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
-  work(0);
-  for (auto &th : pool) th.join();
+  host_parallel_for(nt, work);
   return BGK_OK;
 }
 
@@ -715,10 +793,6 @@ int bgk_host_copy(void *dst, const void *src, int64_t bytes, int nthreads) {
     work(0);
     return BGK_OK;
   }
-  std::vector<std::thread> pool;
-  pool.reserve(nt - 1);
-  for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
-  work(0);
-  for (auto &th : pool) th.join();
+  host_parallel_for(nt, work);
   return BGK_OK;
 }
