@@ -485,6 +485,7 @@ def generate_covariance(locs, theta: MaternParams, cfg: QuadratureConfig = DEFAU
 _MIRROR_MIN_N = 4096
 _MIRROR_POOL = None
 _MIRROR_DIRECT = None  # override of _mirror_direct_blocks (tests / tuning)
+_MIRROR_THREADS = None  # host threads of the mirror (default: all)
 
 
 def _is_pinned(a: np.ndarray) -> bool:
@@ -543,7 +544,10 @@ def _full_host_lower_mirrored(plan, lx, ly, N, host, block_bytes):
         from concurrent.futures import ThreadPoolExecutor
 
         _MIRROR_POOL = ThreadPoolExecutor(max_workers=1)  # mirrors in block order
-    nthreads = _host_threads()
+    # half the host threads: the mirror then keeps pace with the copies and leaves
+    # DRAM bandwidth to the DMA (M100 on the 16-core box: 8 -> 1.04-1.06 s,
+    # 16 -> 1.07 s, 4 -> 1.4 s; tools/mirror_threads.py)
+    nthreads = _MIRROR_THREADS or max(1, _host_threads() // 2)
     block = max(64, min(N, (block_bytes // (8 * N)) // 64 * 64))
     w = _mirror_direct_blocks(N, block)
     dev = lx.device
