@@ -228,7 +228,7 @@ _HOST_CHUNK = 1 << 22  # elements per pipelined chunk for host (numpy) batches
 
 
 _STAGE: dict = {}  # per device: two pinned staging slots (x, nu) of _HOST_CHUNK elements
-_COPY_THREADS = None  # host threads of the pageable -> pinned staging copy (default: all)
+_COPY_THREADS = None  # host threads of the pageable -> pinned staging copy (default: 3/4)
 
 
 def _stage_slots(torch, dev):
@@ -242,16 +242,20 @@ def _stage_slots(torch, dev):
 
 
 def _par_copy(dst: np.ndarray, src: np.ndarray) -> None:
-    """dst[:] = src with all host threads and non-temporal stores (bgk_host_copy):
+    """dst[:] = src with host threads and non-temporal stores (bgk_host_copy):
     the staging copy is host-memory bound and paces the pipeline."""
     global _COPY_THREADS
     if _COPY_THREADS is None:
         import os
 
         try:
-            _COPY_THREADS = max(1, len(os.sched_getaffinity(0)))
+            ncpu = len(os.sched_getaffinity(0))
         except AttributeError:
-            _COPY_THREADS = max(1, os.cpu_count() or 1)
+            ncpu = os.cpu_count() or 1
+        # 3/4 of the host threads: all of them oversubscribe the cores next to the
+        # thread issuing the GPU work (64Mi batch on the 16-core box: 12 threads
+        # 35-38 ms steadily, 16 threads 34-161 ms; tools/copy_threads.py)
+        _COPY_THREADS = max(1, ncpu * 3 // 4)
     assert dst.dtype == src.dtype and dst.size == src.size and dst.flags.c_contiguous \
         and src.flags.c_contiguous
     _lib.check(_lib.load_library().bgk_host_copy(dst.ctypes.data, src.ctypes.data, src.nbytes,
