@@ -67,6 +67,22 @@ def test_argument_validation_without_gpu(L):
     # empty work is a no-op success (no launch)
     assert L.bgk_matern_tile(ctypes.byref(plan), None, None, 0, None, None, 5, None, 5, 0, None) == 0
     big = _lib.BgkConfig(0.0, 9.0, 5000, 0.1, 15000, 2.0 ** -52)
+    assert L.bgk_matern_plan_init(ctypes.byref(plan), 1.0, 0.1, 1.5, ctypes.byref(cfg)) == 0
+    # multi-GPU peer entry points: owners / rank / ranges checked before any launch
+    N, G = 1000, 2
+    T = -(-N // 64)
+    starts = (ctypes.c_int64 * 3)(0, 8, T)
+    bases = (ctypes.c_void_p * 2)(1, 2)
+    assert L.bgk_matern_covariance_peer_band(ctypes.byref(plan), None, None, N, G, starts, bases,
+                                             2, None) == -1  # rank outside [0, G)
+    assert b"rank" in L.bgk_last_error()
+    bad = (ctypes.c_int64 * 3)(0, 8, T + 1)
+    assert L.bgk_matern_covariance_peer_band(ctypes.byref(plan), None, None, N, G, bad, bases,
+                                             0, None) == -1
+    assert L.bgk_matern_covariance_peer(ctypes.byref(plan), None, None, N, G, starts, bases, 0,
+                                        T * (T + 1) // 2 + 1, None) == -1  # tile range
+    assert L.bgk_matern_covariance_peer(ctypes.byref(plan), None, None, N, G, starts, bases, 0,
+                                        0, None) == 0  # empty range: no-op
     assert L.bgk_matern_plan_init(ctypes.byref(plan), 1.0, 0.1, 1.5, ctypes.byref(big)) == -3
 
 
