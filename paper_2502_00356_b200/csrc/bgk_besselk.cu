@@ -63,6 +63,9 @@ constexpr int kBkChunkBytes = kBkChunk * (8 + 8 + 4 + 2 + 1 + 1);  // + 1: keeps
 #ifndef BGK_BK_XBITS
 #define BGK_BK_XBITS 2  // window table: 2^XBITS x cells per octave
 #endif
+#ifndef BGK_BK_NODE_I2F
+#define BGK_BK_NODE_I2F 0  // A/B on B200: 1 -> 1.521 vs 0 -> 1.511 ms (the Matern loop gains, this one not)
+#endif
 #ifndef BGK_BK_NODE_UNROLL
 #define BGK_BK_NODE_UNROLL 2
 #endif
@@ -205,8 +208,12 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
     P *= E;
     Qs *= Ei;
     const double tt = fma(y, kExpK[0], kExpK[6]);
-    const double nd = tt - kExpK[6];
     const int nn = __double2loint(tt);
+#if BGK_BK_NODE_I2F
+    const double nd = __int2double_rn(nn);  // conversion pipe, exact (= tt - magic)
+#else
+    const double nd = tt - kExpK[6];
+#endif
     const double r = fma(nd, -kExpK[1], y);
     double q = fma(r, kExpK[3], kExpK[4]);
     q = fma(q, r, 0.5);
