@@ -78,6 +78,17 @@ int bgk_besselk_batch(const double *x, const double *nu, int64_t n, const bgk_co
 /* Temme starting sums (s0, s1, terms) with K_mu = s0, K_{mu+1} = (2/x) s1.
  * Replaces kernels.temme_sums (kernels.py:230-270) as called by
  * besselk.temme_pair (besselk.py:94-101).  terms may be NULL. */
+/* Introspection of the fast integral path's node windows (tests: the window table
+ * must cover every node the reference keeps).  Per element: m = the anchor node
+ * the kernel uses, [lo, hi] = the nodes it sums; m = -1 when the element does
+ * not take the fast windowed path (series, reference path).  The _host variant
+ * runs on the CPU with the host anchor (fp32 asinhf); the device variant runs
+ * the kernel's own classify + fast fp32 anchor on device pointers. */
+int bgk_besselk_windows_host(const double *x, const double *nu, int64_t n,
+                             const bgk_config *cfg, int32_t *m, int32_t *lo, int32_t *hi);
+int bgk_besselk_windows(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
+                        int32_t *m, int32_t *lo, int32_t *hi, void *stream);
+
 int bgk_temme_sums_batch(const double *x, const double *mu, int64_t n, const bgk_config *cfg,
                          double *s0, double *s1, int64_t *terms, void *stream);
 
@@ -286,6 +297,13 @@ int bgk_sqrt_rn_check(const double *x, int64_t n, double *fast, double *ref, voi
 /* Number of kernel launches issued by this library since load (for bench.py's
  * gpu_launches accounting). */
 int64_t bgk_launch_count(void);
+
+/* Test hook for the per-device caches (shared-memory opt-ins, uploaded BesselK
+ * tables, task counters): they are keyed by (current device + alias).  Setting a
+ * new alias makes the next launches see a device the library has not configured
+ * yet, so a one-GPU box exercises the cache-miss path a second GPU would take.
+ * Returns the previous alias.  Not for production use. */
+int bgk_debug_set_device_alias(int alias);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,8 @@ _int = ctypes.c_int
 # symbol -> (restype, argtypes); kept in sync with include/besselgp_b200.h
 SIGNATURES = {
     "bgk_besselk_batch": (_int, [_vp, _vp, _i64, ctypes.POINTER(BgkConfig), _int, _vp, _vp, _vp, _vp]),
+    "bgk_besselk_windows_host": (_int, [_vp, _vp, _i64, ctypes.POINTER(BgkConfig), _vp, _vp, _vp]),
+    "bgk_besselk_windows": (_int, [_vp, _vp, _i64, ctypes.POINTER(BgkConfig), _vp, _vp, _vp, _vp]),
     "bgk_temme_sums_batch": (_int, [_vp, _vp, _i64, ctypes.POINTER(BgkConfig), _vp, _vp, _vp, _vp]),
     "bgk_log_integrand_batch": (_int, [_vp, _vp, _vp, _i64, _int, _vp, _vp]),
     "bgk_matern_plan_size": (ctypes.c_size_t, []),
@@ -110,6 +112,7 @@ SIGNATURES = {
     "bgk_last_error": (ctypes.c_char_p, []),
     "bgk_abi_version": (_int, []),
     "bgk_launch_count": (_i64, []),
+    "bgk_debug_set_device_alias": (_int, [_int]),
     "bgk_fp64_probe": (_int, [_vp, _i64, _int, _vp, ctypes.POINTER(ctypes.c_double)]),
     "bgk_sqrt_rn_check": (_int, [_vp, _i64, _vp, _vp, _vp]),
     "bgk_matern_covariance_peer": (_int, [ctypes.POINTER(BgkMaternPlan), _vp, _vp, _i64, _int,

@@ -17,6 +17,7 @@ from __future__ import annotations
 import ctypes
 import enum
 import math
+import threading
 from dataclasses import dataclass, field
 from typing import NamedTuple
 
@@ -228,6 +229,10 @@ _HOST_CHUNK = 1 << 22  # elements per pipelined chunk for host (numpy) batches
 
 
 _STAGE: dict = {}  # per device: two pinned staging slots (x, nu) of _HOST_CHUNK elements
+# per device: held for a whole pipelined call, so two host threads never stage into
+# the same pinned slots (ctypes releases the GIL inside bgk_host_copy)
+_STAGE_LOCKS: dict = {}
+_STAGE_LOCKS_GUARD = threading.Lock()
 _COPY_THREADS = None  # host threads of the pageable -> pinned staging copy (default: 3/4)
 
 
@@ -274,6 +279,13 @@ def _bessel_k_host_pipelined(xa, na, cfg, route, validate):
     nf = np.ascontiguousarray(na).reshape(-1)
     n = xf.size
     dev = torch.device("cuda", torch.cuda.current_device())
+    with _STAGE_LOCKS_GUARD:
+        lock = _STAGE_LOCKS.setdefault(dev.index, threading.Lock())
+    with lock:
+        return _host_pipeline_locked(torch, dev, xf, nf, n, shape, cfg, route, validate)
+
+
+def _host_pipeline_locked(torch, dev, xf, nf, n, shape, cfg, route, validate):
     out_l = torch.empty(n, dtype=torch.float64, pin_memory=True)
     out_k = torch.empty(n, dtype=torch.float64, pin_memory=True)
     out_p = torch.empty(n, dtype=torch.uint8, pin_memory=True)

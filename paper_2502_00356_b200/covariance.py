@@ -143,13 +143,22 @@ class CovarianceMatrix:
         ts, N = self.tile_size, self.N
         r0, c0 = p * ts, q * ts
         m, n = min(ts, N - r0), min(ts, N - c0)
+        if not (0 <= r0 < N and 0 <= c0 < N):
+            raise DomainError(f"tile ({p}, {q}) lies outside the {N} x {N} matrix")
         if self.layout == "full":
+            if not (self.row_begin <= r0 and r0 + m <= self.row_end):
+                raise DomainError(f"tile row {p} (rows [{r0}, {r0 + m})) is outside this "
+                                  f"block's rows [{self.row_begin}, {self.row_end})")
             a = self.to_numpy()
             return a[r0 - self.row_begin:r0 - self.row_begin + m, c0:c0 + n]
         if q > p:
             return self.tile(q, p).T
         l = p * (p + 1) // 2 + q - self.tile_begin
-        return self.to_numpy()[l].T[:m, :n]
+        data = self.to_numpy()
+        if not 0 <= l < data.shape[0]:
+            raise DomainError(f"tile ({p}, {q}) is outside this shard's tile range "
+                              f"[{self.tile_begin}, {self.tile_begin + data.shape[0]})")
+        return data[l].T[:m, :n]
 
     # ---- CVMX binary format: 'CVMX', u32 version=1, u64 N, col-major f64 ----
     def write_cvmx(self, path: str) -> None:
@@ -237,8 +246,9 @@ def _dev(a, device=None):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(device or "cuda")
 
 
-def _coords(locs):
-    """(x, y) float64 CUDA tensors from a LocationSet, an (N,2) array or tensor."""
+def _coords(locs, device=None):
+    """(x, y) float64 CUDA tensors from a LocationSet, an (N,2) array or tensor, on
+    ``device`` (default: a CUDA tensor's own device, else the current device)."""
     _lib.lib()  # BackendUnavailable (not a CPU fallback) when there is no GPU / library
     torch = _torch()
     if isinstance(locs, LocationSet):
@@ -247,7 +257,9 @@ def _coords(locs):
         c = locs
     if isinstance(c, torch.Tensor):
         c = c.to(dtype=torch.float64)
-        if not c.is_cuda:
+        if device is not None:
+            c = c.to(device)
+        elif not c.is_cuda:
             c = c.cuda()
         if c.ndim != 2 or c.shape[1] != 2:
             raise DomainError(f"coords must have shape (N, 2), got {tuple(c.shape)}")
@@ -255,8 +267,53 @@ def _coords(locs):
     c = np.ascontiguousarray(c, dtype=np.float64)
     if c.ndim != 2 or c.shape[1] != 2:
         raise DomainError(f"coords must have shape (N, 2), got {c.shape}")
-    t = torch.from_numpy(np.ascontiguousarray(c.T)).cuda()
+    t = torch.from_numpy(np.ascontiguousarray(c.T)).to(device if device is not None else "cuda")
     return t[0], t[1]
+
+
+def _target_device(out, device, locs):
+    """The device a covariance call runs on: a CUDA ``out``'s, else ``device``, else a
+    CUDA location tensor's, else the current device."""
+    _lib.lib()  # BackendUnavailable (not a CPU fallback) when there is no GPU / library
+    torch = _torch()
+    if isinstance(out, torch.Tensor) and out.is_cuda:
+        if device is not None and torch.device(device) != out.device:
+            raise DomainError(f"out is on {out.device} but device={device!r} was requested")
+        return out.device
+    if device is not None:
+        d = torch.device(device)
+        if d.type != "cuda":
+            raise DomainError(f"device must be a CUDA device, got {device!r}")
+        return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
+    c = locs.coords if isinstance(locs, LocationSet) else locs
+    if isinstance(c, torch.Tensor) and c.is_cuda:
+        return c.device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _check_device_out(buf, shape, dev):
+    torch = _torch()
+    if not (isinstance(buf, torch.Tensor) and buf.dtype == torch.float64 and buf.device == dev
+            and tuple(buf.shape) == tuple(shape) and buf.is_contiguous()):
+        got = (f"{tuple(buf.shape)} {buf.dtype} on {buf.device}, contiguous={buf.is_contiguous()}"
+               if isinstance(buf, torch.Tensor) else type(buf).__name__)
+        raise DomainError(f"out must be a contiguous {tuple(shape)} float64 tensor on {dev}; "
+                          f"got {got}")
+
+
+def _zero_tile_padding(buf, N, ts, l0, l1):
+    """Zero the entries of packed lower tiles that lie beyond N (edge tiles of the
+    last tile row and column); the kernel writes only the m x n valid part."""
+    r = N % ts
+    if r == 0 or l1 <= l0:
+        return
+    T = -(-N // ts)
+    a, b = max(l0, T * (T - 1) // 2), min(l1, T * (T + 1) // 2)  # tile row p = T - 1
+    if a < b:
+        buf[a - l0:b - l0, :, r:] = 0.0   # column-major inside a tile: [l, col, row]
+    last = T * (T + 1) // 2 - 1           # the corner tile (T-1, T-1)
+    if l0 <= last < l1:
+        buf[last - l0, r:, :] = 0.0
 
 
 def _tile_launch(plan, rx, ry, cx, cy, out, ld, layout):
@@ -333,8 +390,9 @@ def generate_tile(spec: TileSpec, rows_locs, cols_locs, theta: MaternParams,
     are CUDA tensors.  ``layout="col"`` stores it column-major (a Fortran-ordered
     numpy array / a transposed tensor view), as SPEC.md:283 keeps tiles."""
     torch = _torch()
-    rx, ry = _coords(rows_locs)
-    cx, cy = _coords(cols_locs)
+    dev = _target_device(None, None, rows_locs)
+    rx, ry = _coords(rows_locs, dev)
+    cx, cy = _coords(cols_locs, dev)
     if rx.numel() != spec.rows or cx.numel() != spec.cols:
         raise DomainError("location slices are inconsistent with the TileSpec dims")
     on_device = any(isinstance(v, torch.Tensor) and v.is_cuda for v in (rows_locs, cols_locs))
@@ -407,19 +465,27 @@ def generate_covariance(locs, theta: MaternParams, cfg: QuadratureConfig = DEFAU
         N = int(locs.shape[0])
     if tile_size < 1:
         raise DomainError("tile_size must be at least 1")
-    lx, ly = _coords(locs)
+    dev = _target_device(out, device, locs)
+    lx, ly = _coords(locs, dev)
     plan = matern_plan(theta, cfg)
 
     if layout == "lower_tiles":
-        l0, l1 = tiles if tiles is not None else (0, lower_tile_count(N, tile_size))
+        ntiles = lower_tile_count(N, tile_size)
+        l0, l1 = tiles if tiles is not None else (0, ntiles)
+        if not (0 <= l0 <= l1 <= ntiles):
+            raise DomainError(f"tiles must satisfy 0 <= l0 <= l1 <= {ntiles}, got {(l0, l1)}")
         shape = (l1 - l0, tile_size, tile_size)
-        if out is None:
-            host = device is None
-            # zero-filled so the padding of edge tiles (entries beyond N) is defined
-            buf = torch.zeros(shape, dtype=torch.float64, device=lx.device if host else device)
+        host = not (isinstance(out, torch.Tensor) and out.is_cuda) and (out is not None
+                                                                         or device is None)
+        if out is not None and not host:
+            buf = out
+            _check_device_out(buf, shape, dev)
         else:
-            host = not (isinstance(out, torch.Tensor) and out.is_cuda)
-            buf = torch.zeros(shape, dtype=torch.float64, device=lx.device) if host else out
+            buf = torch.empty(shape, dtype=torch.float64, device=dev)
+            if out is not None and (out.shape != shape or out.dtype != np.float64):
+                raise DomainError(f"out must be a {shape} float64 array")
+        # the padding of edge tiles (entries beyond N) is defined: zero
+        _zero_tile_padding(buf, N, tile_size, l0, l1)
         if l1 > l0 and N:
             _lower_launch(plan, lx, ly, N, tile_size, l0, l1, buf)
         data = buf
@@ -442,9 +508,8 @@ def generate_covariance(locs, theta: MaternParams, cfg: QuadratureConfig = DEFAU
         out is None and device is not None)
     if device_out:
         buf = out if out is not None else torch.empty((nrows, N), dtype=torch.float64,
-                                                      device=device)
-        if tuple(buf.shape) != (nrows, N) or not buf.is_contiguous():
-            raise DomainError(f"out must be a contiguous ({nrows}, {N}) float64 tensor")
+                                                      device=dev)
+        _check_device_out(buf, (nrows, N), dev)
         if nrows and N:
             _cov_launch(plan, lx, ly, N, r0, r1, buf, N, _lib.LAYOUT_ROW_MAJOR)
         return CovarianceMatrix(N=N, data=buf, tile_size=tile_size, row_begin=r0, row_end=r1,

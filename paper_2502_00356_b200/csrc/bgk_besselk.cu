@@ -19,10 +19,12 @@
 //       ln K = a t_a - ln2 - x c_a + ln(h acc)
 //
 // Node window: a host-built table over (log x, nu) cells gives, relative to the
-// anchor, how far up and down the terms stay above e^-40 of the anchor term
-// (maximised over a 5 x 5 sample of the cell, no margin: a node just outside
-// the sampled extent is within ~e^-38 of the anchor term); each lane
-// sums its window [m - D, m + U] as one ascending sequence.  The reference's
+// anchor, how far up and down the terms stay above e^-41 of the anchor term
+// (maximised over a 17 x 17 sample of the cell, edges included; the extra e^-1
+// below the e^-40 cut covers the variation between samples: every node the
+// reference keeps at e^-40 of the grid max lies inside, checked on a denser
+// sample by tests/test_bk_window_table.py); each lane sums its window
+// [m - D, m + U] as one ascending sequence.  The reference's
 // walk also keeps terms in (e^-46, e^-40]: each is < 4e-18 of the sum, so
 // dropping them is below an ulp.  Elements outside the table's range use the
 // full grid [0, bins].
@@ -78,6 +80,14 @@ constexpr int kBkNodeUnroll = BGK_BK_NODE_UNROLL;
 #define BGK_BK_MARGIN 0  // nodes added to each side of the sampled window extents (A/B on
                          // B200: 0 -> 1.606 ms, 1 -> 1.661 ms; max|d ln K| unchanged, 5.7e-14)
 #endif
+#ifndef BGK_BK_WSAMP
+#define BGK_BK_WSAMP 16  // window table: (WSAMP+1)^2 samples per cell, edges included
+#endif
+#ifndef BGK_BK_WCUT
+#define BGK_BK_WCUT 41.0  // window table: keep nodes within e^-WCUT of the anchor term (the
+                          // reference's window is e^-40 of the max; the extra 1 covers the
+                          // variation between samples: tests/test_bk_window_table.py)
+#endif
 #ifndef BGK_BK_NUSTEP
 #define BGK_BK_NUSTEP 2  // window table: nu cells per unit of nu
 #endif
@@ -109,6 +119,16 @@ struct BkArgs {
   float t0f, hinvf, binsf;  // anchor_node_fast's fp32 constants
 };
 
+// Unclamped x-cell key: exponent + top kXBits mantissa bits, relative to 2^-6.
+__host__ __device__ inline int x_cell_key(double x) {
+  uint64_t b;
+#ifdef __CUDA_ARCH__
+  b = (uint64_t)__double_as_longlong(x);
+#else
+  std::memcpy(&b, &x, 8);
+#endif
+  return (int)(b >> (52 - kXBits)) - kXKeyBase;
+}
 __host__ __device__ inline int x_cell(double x) {
   uint64_t b;
 #ifdef __CUDA_ARCH__
@@ -151,16 +171,37 @@ __device__ __forceinline__ int anchor_node_fast(double x, double a, float t0f, f
   return (int)fm;
 }
 
+// The fast path's window word for an integral-route element (0: not on the fast
+// path -> reference port): the host-built table's U | D << 16 for cells proven
+// underflow-free, the full grid for x outside the table when every exponent stays
+// >= -600, else 0.  Shared by the kernel's classify pass and the window
+// introspection exports (bgk_besselk_windows{,_host}).
+__host__ __device__ inline uint32_t bk_window_word(double x, double a, int table_ok,
+                                                   double tmax, double cmax, int bins,
+                                                   const uint32_t *win) {
+  uint32_t w = 0;
+  if (table_ok && a * tmax <= 600.0) {  // E^{+-j} cannot overflow
+    const int key = x_cell_key(x);
+    if (key >= 0 && key < kXCells && a * (double)kNuStep < (double)(kNuCells - 1)) {
+#ifdef __CUDA_ARCH__
+      w = __ldg(win + key * kNuCells + nu_cell(a));
+#else
+      w = win[key * kNuCells + nu_cell(a)];
+#endif
+      if (w == 0xffffffffu) w = 0;  // cell not proven underflow-free: reference path
+    } else if (x * cmax <= 600.0) {
+      w = (uint32_t)bins | ((uint32_t)bins << 16);  // full grid, exponents >= -600
+    }
+  }
+  return w;
+}
+
 __device__ __forceinline__ int ld_u16_volatile(const uint16_t *p) {
   unsigned short v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
   return v;
 }
 
-__device__ __forceinline__ bool in_table(double x, double a) {
-  const int key = (int)((uint64_t)__double_as_longlong(x) >> (52 - kXBits)) - kXKeyBase;
-  return key >= 0 && key < kXCells && a * (double)kNuStep < (double)(kNuCells - 1);
-}
 
 // Fast fixed-window quadrature (see file header).  Requires t0 >= 0 and an
 // element inside the window table (its window keeps every exponent above
@@ -237,6 +278,9 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
 // The Temme path (x < threshold: 0.08% of the BK elements) out of line, so its
 // long chain does not take registers from the fast path's loop.
 __device__ __noinline__ double bk_series_log(double x, double nu, double eps, long long cap) {
+  // a non-finite order would saturate the recurrence's step count (floor(inf + 0.5)
+  // -> INT_MAX steps): NaN at once instead (the validated API rejects it anyway)
+  if (!(fabs(nu) <= 1.7976931348623157e308)) return __longlong_as_double(0x7ff8000000000000LL);
   const TemmeConst T = temme_const(nu);
   return temme_series_log_c(x, T, eps, cap);
 }
@@ -291,13 +335,8 @@ __global__ void __launch_bounds__(kBkThreads, BGK_BK_MINBLOCKS) besselk_kernel(c
     uint32_t w = 0;
     if (series) {
       b = 0;
-    } else if (A.table_ok && a * tmax <= 600.0) {  // E^{+-j} cannot overflow
-      if (in_table(x, a)) {
-        w = __ldg(A.win + x_cell(x) * kNuCells + nu_cell(a));
-        if (w == 0xffffffffu) w = 0;  // cell not proven underflow-free: reference path
-      } else if (x * cmax <= 600.0) {
-        w = (uint32_t)A.bins | ((uint32_t)A.bins << 16);  // full grid, exponents >= -600
-      }
+    } else {
+      w = bk_window_word(x, a, A.table_ok, tmax, cmax, A.bins, A.win);
       if (w) {
         const int nw = (int)(w & 0xffff) + (int)(w >> 16) + 1;
         b = 2 * (kMaxPred - min(nw, kMaxPred - 1)) - (a * a <= x ? 1 : 0);
@@ -439,7 +478,7 @@ static void walk_extent_host(double x, double a, double t0, double h, int bins, 
   const double ta = t0 + m * h, ca = c[m];
   const double E = std::exp(a * h), Ei = std::exp(-a * h);
   const double q = (2 * a * ta < 700) ? std::exp(-2 * a * ta) : 0.0;
-  const double tiny = 4.248354255291589e-18 * (1 + q);  // e^-40
+  const double tiny = std::exp(-BGK_BK_WCUT) * (1 + q);
   up = dn = 0;
   double p = 1, qq = 1;
   for (int j = 1; m + j <= bins; ++j) {
@@ -458,8 +497,8 @@ static void walk_extent_host(double x, double a, double t0, double h, int bins, 
   }
 }
 
-// Per (x, nu) cell: U | D << 16, the largest up / down extents over a 5 x 5 sample
-// of the cell (plus BGK_BK_MARGIN nodes).
+// Per (x, nu) cell: U | D << 16, the largest up / down extents over a
+// (WSAMP + 1)^2 sample of the cell, edges included (plus BGK_BK_MARGIN nodes).
 static void build_window_table(double t0, double t1, int bins, uint32_t *win) {
   std::vector<double> c(bins + 1);
   const double h = (t1 - t0) / bins;
@@ -473,10 +512,12 @@ static void build_window_table(double t0, double t1, int bins, uint32_t *win) {
       const double nlo = ni / (double)kNuStep;
       const double nhi = nlo + 1.0 / kNuStep;
       int U = 0, D = 0;
-      for (int sx = 0; sx <= 4; ++sx)
-        for (int sn = 0; sn <= 4; ++sn) {
-          const double xv = lo + (hi - lo) * sx / 4.0 * 0.9999;
-          const double nv = nlo + (nhi - nlo) * sn / 4.0 * 0.9999;
+      for (int sx = 0; sx <= BGK_BK_WSAMP; ++sx)
+        for (int sn = 0; sn <= BGK_BK_WSAMP; ++sn) {
+          const double xv = sx == BGK_BK_WSAMP ? std::nextafter(hi, 0.0)
+                                               : lo + (hi - lo) * sx / (double)BGK_BK_WSAMP;
+          const double nv = sn == BGK_BK_WSAMP ? std::nextafter(nhi, 0.0)
+                                               : nlo + (nhi - nlo) * sn / (double)BGK_BK_WSAMP;
           int up, dn;
           walk_extent_host(xv, nv, t0, h, bins, c.data(), up, dn);
           U = std::max(U, up);
@@ -506,21 +547,23 @@ static void build_window_table(double t0, double t1, int bins, uint32_t *win) {
 // ---------------------------------------------------------------------------------
 // launchers (called from bgk_capi.cpp)
 // ---------------------------------------------------------------------------------
-// Device copies of the node-window table, one per (t0, t1, bins), built on the
-// host and uploaded once (12 KB each); kept for the life of the process.
+// Device copies of the node-window table, one per (device, t0, t1, bins), built
+// on the host and uploaded once per device (12 KB each); kept for the life of the
+// process.  The key is bgk_device_key(): a pointer uploaded on one device is never
+// handed to a launch on another.
 struct PredEntry {
+  int device_key;
   double t0, t1;
   long long bins;
   uint32_t *dev;  // window table, then the {cosh t_k, ln w_k} node table
   double2 *cw;
 };
 
-int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
-                       int route, double *log_k, double *k, uint8_t *path, cudaStream_t stream) {
-  if (n == 0) return 0;
-  static std::mutex mu;
-  static std::vector<PredEntry> cache;
-  bgk::BkArgs A;
+namespace {
+constexpr int64_t kMaxTable = 8191;  // 128 KB of shared memory ({c, ln w} pairs)
+
+void bk_fill_args(bgk::BkArgs &A, const double *x, const double *nu, int64_t n,
+                  const bgk_config *cfg, int route, double *log_k, double *k, uint8_t *path) {
   A.x = x;
   A.nu = nu;
   A.log_k = log_k;
@@ -538,55 +581,151 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
   A.t0f = (float)A.t0;
   A.hinvf = (float)(1.0 / A.h);
   A.binsf = (float)A.bins;
-  const int64_t kMaxTable = 8191;  // 128 KB of shared memory ({c, ln w} pairs)
   A.table_ok = (cfg->t_lower >= 0.0 && cfg->bins <= kMaxTable) ? 1 : 0;
   A.win = nullptr;
   A.cwg = nullptr;
-  if (A.table_ok) {
-    std::lock_guard<std::mutex> lock(mu);
-    for (const PredEntry &e : cache)
-      if (e.t0 == cfg->t_lower && e.t1 == cfg->t_upper && e.bins == cfg->bins) {
-        A.win = e.dev;
-        A.cwg = e.cw;
-      }
-    if (!A.win) {
-      const size_t nwin = (size_t)bgk::kXCells * bgk::kNuCells;
-      const size_t nwin_pad = (nwin + 3) & ~(size_t)3;  // 16-byte aligned node table
-      const int bins = (int)cfg->bins;
-      std::vector<uint32_t> host(nwin_pad + 4 * (size_t)(bins + 1), 0u);
-      bgk::build_window_table(cfg->t_lower, cfg->t_upper, bins, host.data());
-      // node table exactly as the reference's caller builds it: t_k = t0 + k h,
-      // cosh via the host libm (what numba calls), trapezoid weight in the exponent
-      const double h = (cfg->t_upper - cfg->t_lower) / (double)bins;
-      double *cwh = reinterpret_cast<double *>(host.data() + nwin_pad);
-      for (int k = 0; k <= bins; ++k) {
-        cwh[2 * k] = std::cosh(cfg->t_lower + (double)k * h);
-        // weight 1/2 at the ends as an exponent adjustment (see fixed_window_fast)
-        const uint64_t wbits = (k == 0 || k == bins) ? (uint64_t)(uint32_t)(-(1 << 20)) : 0u;
-        std::memcpy(&cwh[2 * k + 1], &wbits, 8);
-      }
-      uint32_t *dev = nullptr;
-      const size_t bytes = host.size() * sizeof(uint32_t);
-      cudaError_t err = cudaMalloc(&dev, bytes);
-      if (err == cudaSuccess) err = cudaMemcpy(dev, host.data(), bytes, cudaMemcpyHostToDevice);
-      if (err != cudaSuccess) {
-        bgk_set_error("besselk prediction table upload: %s", cudaGetErrorString(err));
-        return BGK_ERR_CUDA;
-      }
-      double2 *cwd = reinterpret_cast<double2 *>(dev + nwin_pad);
-      cache.push_back({cfg->t_lower, cfg->t_upper, cfg->bins, dev, cwd});
-      A.win = dev;
-      A.cwg = cwd;
-    }
+}
+
+// Host image of the tables: the window table (padded to 16 B), then the node table
+// {cosh t_k, weight exponent adjust} exactly as the reference's caller builds it:
+// t_k = t0 + k h, cosh via the host libm (what numba calls).
+size_t bk_host_tables(const bgk_config *cfg, std::vector<uint32_t> &host) {
+  const size_t nwin = (size_t)bgk::kXCells * bgk::kNuCells;
+  const size_t nwin_pad = (nwin + 3) & ~(size_t)3;  // 16-byte aligned node table
+  const int bins = (int)cfg->bins;
+  host.assign(nwin_pad + 4 * (size_t)(bins + 1), 0u);
+  bgk::build_window_table(cfg->t_lower, cfg->t_upper, bins, host.data());
+  const double h = (cfg->t_upper - cfg->t_lower) / (double)bins;
+  double *cwh = reinterpret_cast<double *>(host.data() + nwin_pad);
+  for (int k = 0; k <= bins; ++k) {
+    cwh[2 * k] = std::cosh(cfg->t_lower + (double)k * h);
+    // weight 1/2 at the ends as an exponent adjustment (see fixed_window_fast)
+    const uint64_t wbits = (k == 0 || k == bins) ? (uint64_t)(uint32_t)(-(1 << 20)) : 0u;
+    std::memcpy(&cwh[2 * k + 1], &wbits, 8);
   }
+  return nwin_pad;
+}
+
+// Device copies of the tables, one per (device, t0, t1, bins), uploaded once per
+// device (12 KB + the node table); kept for the life of the process.
+int bk_device_tables(const bgk_config *cfg, bgk::BkArgs &A) {
+  static std::mutex mu;
+  static std::vector<PredEntry> cache;
+  if (!A.table_ok) return BGK_OK;
+  const int dev_key = bgk_device_key(nullptr);
+  std::lock_guard<std::mutex> lock(mu);
+  for (const PredEntry &e : cache)
+    if (e.device_key == dev_key && e.t0 == cfg->t_lower && e.t1 == cfg->t_upper &&
+        e.bins == cfg->bins) {
+      A.win = e.dev;
+      A.cwg = e.cw;
+      return BGK_OK;
+    }
+  std::vector<uint32_t> host;
+  const size_t nwin_pad = bk_host_tables(cfg, host);
+  uint32_t *dev = nullptr;
+  const size_t bytes = host.size() * sizeof(uint32_t);
+  cudaError_t err = cudaMalloc(&dev, bytes);
+  if (err == cudaSuccess) err = cudaMemcpy(dev, host.data(), bytes, cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    bgk_set_error("besselk prediction table upload: %s", cudaGetErrorString(err));
+    return BGK_ERR_CUDA;
+  }
+  double2 *cwd = reinterpret_cast<double2 *>(dev + nwin_pad);
+  cache.push_back({dev_key, cfg->t_lower, cfg->t_upper, cfg->bins, dev, cwd});
+  A.win = dev;
+  A.cwg = cwd;
+  return BGK_OK;
+}
+
+// The window an element is summed over, as the kernel decides it (anchor: the host
+// fp32 asinhf on the CPU, the kernel's fast fp32 anchor on the device).
+__host__ __device__ inline void bk_window_of(double x, double nu, const bgk::BkArgs &A,
+                                             double cmax, bool device_anchor, int32_t &m,
+                                             int32_t &lo, int32_t &hi) {
+  m = lo = hi = -1;
+  const double a = fabs(nu);
+  const bool series = (A.route == 1) || (A.route == 0 && x < A.thr);
+  if (series) return;
+  const double tmax = fmax(fabs(A.t0), fabs(A.t1));
+  const uint32_t w = bgk::bk_window_word(x, a, A.table_ok, tmax, cmax, A.bins, A.win);
+  if (!w) return;
+#ifdef __CUDA_ARCH__
+  const int mm = device_anchor ? bgk::anchor_node_fast(x, a, A.t0f, A.hinvf, A.binsf)
+                               : bgk::anchor_node(x, a, A.t0, A.h, A.bins);
+#else
+  (void)device_anchor;
+  const int mm = bgk::anchor_node(x, a, A.t0, A.h, A.bins);
+#endif
+  const int U = min((int)(w & 0xffff), A.bins - mm), D = min((int)(w >> 16), mm);
+  m = mm;
+  lo = mm - D;
+  hi = mm + U;
+}
+
+__global__ void bk_windows_kernel(const bgk::BkArgs A, int32_t *m, int32_t *lo, int32_t *hi) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= A.n) return;
+  const double cmax = A.table_ok ? A.cwg[A.bins].x : 0.0;
+  int32_t a, b, c;
+  bk_window_of(A.x[i], A.nu[i], A, cmax, true, a, b, c);
+  m[i] = a;
+  lo[i] = b;
+  hi[i] = c;
+}
+}  // namespace
+
+extern "C" int bgk_besselk_windows_host(const double *x, const double *nu, int64_t n,
+                                        const bgk_config *cfg, int32_t *m, int32_t *lo,
+                                        int32_t *hi) {
+  if (!cfg || n < 0 || (n > 0 && (!x || !nu || !m || !lo || !hi)) || cfg->bins < 1 ||
+      !(cfg->t_upper > cfg->t_lower)) {
+    bgk_set_error("bgk_besselk_windows_host: bad arguments");
+    return BGK_ERR_INVALID;
+  }
+  bgk::BkArgs A;
+  bk_fill_args(A, x, nu, n, cfg, 0, nullptr, nullptr, nullptr);
+  std::vector<uint32_t> host;
+  double cmax = 0.0;
+  if (A.table_ok) {
+    const size_t nwin_pad = bk_host_tables(cfg, host);
+    A.win = host.data();
+    cmax = reinterpret_cast<const double *>(host.data() + nwin_pad)[2 * cfg->bins];
+  }
+  for (int64_t i = 0; i < n; ++i) bk_window_of(x[i], nu[i], A, cmax, false, m[i], lo[i], hi[i]);
+  return BGK_OK;
+}
+
+extern "C" int bgk_besselk_windows(const double *x, const double *nu, int64_t n,
+                                   const bgk_config *cfg, int32_t *m, int32_t *lo, int32_t *hi,
+                                   void *stream) {
+  if (!cfg || n < 0 || (n > 0 && (!x || !nu || !m || !lo || !hi)) || cfg->bins < 1 ||
+      !(cfg->t_upper > cfg->t_lower)) {
+    bgk_set_error("bgk_besselk_windows: bad arguments");
+    return BGK_ERR_INVALID;
+  }
+  if (n == 0) return BGK_OK;
+  bgk::BkArgs A;
+  bk_fill_args(A, x, nu, n, cfg, 0, nullptr, nullptr, nullptr);
+  if (int rc = bk_device_tables(cfg, A)) return rc;
+  bk_windows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(A, m, lo, hi);
+  bgk_note_launch();
+  return bgk_check_launch("bk_windows_kernel");
+}
+
+int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
+                       int route, double *log_k, double *k, uint8_t *path, cudaStream_t stream) {
+  if (n == 0) return 0;
+  bgk::BkArgs A;
+  bk_fill_args(A, x, nu, n, cfg, route, log_k, k, path);
+  if (int rc = bk_device_tables(cfg, A)) return rc;
   const size_t chunk_bytes = (size_t)bgk::kBkChunkBytes;
   size_t smem = sizeof(double2) * (A.table_ok ? (size_t)cfg->bins + 1 : 0) + chunk_bytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(bgk::besselk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double2) * (kMaxTable + 1) + chunk_bytes));
-    attr_set = true;
-  }
+  // opt in once per device for the largest table (so every bins <= kMaxTable fits)
+  if (int rc = bgk_ensure_smem_optin((const void *)bgk::besselk_kernel, "besselk_kernel",
+                                     (int)(sizeof(double2) * (kMaxTable + 1) + chunk_bytes)))
+    return rc;
   long long grid = (n + bgk::kBkChunk - 1) / bgk::kBkChunk;
   bgk::besselk_kernel<<<(unsigned)grid, bgk::kBkThreads, smem, stream>>>(A);
   bgk_note_launch();

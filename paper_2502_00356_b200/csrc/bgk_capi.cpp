@@ -271,11 +271,51 @@ int bgk_check_launch(const char *what) {
 
 void bgk_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+namespace {
+std::atomic<int> g_device_alias{0};
+std::mutex g_optin_mu;
+struct OptIn {
+  const void *kernel;
+  int dev;
+  int bytes;
+};
+std::vector<OptIn> g_optins;  // guarded by g_optin_mu
+}  // namespace
+
+int bgk_device_key(int *real_device) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (real_device) *real_device = dev;
+  return dev + g_device_alias.load();
+}
+
+int bgk_ensure_smem_optin(const void *kernel, const char *name, int bytes) {
+  const int key = bgk_device_key(nullptr);
+  std::lock_guard<std::mutex> lock(g_optin_mu);
+  for (const OptIn &o : g_optins)
+    if (o.kernel == kernel && o.dev == key && o.bytes >= bytes) return BGK_OK;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    bgk_set_error("cudaFuncSetAttribute(%s, %d bytes): %s", name, bytes, cudaGetErrorString(e));
+    return BGK_ERR_CUDA;
+  }
+  for (OptIn &o : g_optins)
+    if (o.kernel == kernel && o.dev == key) {
+      o.bytes = bytes;
+      return BGK_OK;
+    }
+  g_optins.push_back({kernel, key, bytes});
+  return BGK_OK;
+}
+
 extern "C" {
 
 const char *bgk_last_error(void) { return g_err; }
 int bgk_abi_version(void) { return BGK_ABI_VERSION; }
 int64_t bgk_launch_count(void) { return g_launches.load(); }
+int bgk_debug_set_device_alias(int alias) { return g_device_alias.exchange(alias); }
 size_t bgk_matern_plan_size(void) { return sizeof(bgk_matern_plan); }
 
 int bgk_besselk_batch(const double *x, const double *nu, int64_t n, const bgk_config *cfg,

@@ -11,6 +11,15 @@ void bgk_set_error(const char *fmt, ...);
 int bgk_check_launch(const char *what);
 void bgk_note_launch();
 
+// Per-device state.  Shared-memory opt-ins, uploaded tables and task counters are
+// per CUDA device: every cache is keyed by bgk_device_key() (the current device,
+// plus a test-only alias offset set by bgk_debug_set_device_alias so a one-GPU
+// box can exercise the cache-miss path), and the opt-in is re-checked per device.
+int bgk_device_key(int *real_device);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) once per (kernel, device,
+// size), under a mutex, return code checked.  0 or BGK_ERR_CUDA.
+int bgk_ensure_smem_optin(const void *kernel, const char *name, int bytes);
+
 // launchers
 int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
                        int route, double *log_k, double *k, uint8_t *path, cudaStream_t stream);
