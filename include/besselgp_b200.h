@@ -78,6 +78,13 @@ int bgk_besselk_batch(const double *x, const double *nu, int64_t n, const bgk_co
 /* Temme starting sums (s0, s1, terms) with K_mu = s0, K_{mu+1} = (2/x) s1.
  * Replaces kernels.temme_sums (kernels.py:230-270) as called by
  * besselk.temme_pair (besselk.py:94-101).  terms may be NULL. */
+/* One (x, nu): ln K into *log_k (a HOST pointer), synchronously on `stream`.  The
+ * inputs and result travel through a per-thread, per-device mapped page-locked
+ * slot (no memcpy calls): one kernel launch + one stream sync.  Same bits as
+ * bgk_besselk_batch.  Backs the scalar drop-in API (besselk.py:94-165). */
+int bgk_besselk_scalar(double x, double nu, const bgk_config *cfg, int route, double *log_k,
+                       void *stream);
+
 /* Introspection of the fast integral path's node windows (tests: the window table
  * must cover every node the reference keeps).  Per element: m = the anchor node
  * the kernel uses, [lo, hi] = the nodes it sums; m = -1 when the element does
@@ -248,6 +255,9 @@ int bgk_matern_covariance_peer_band(const bgk_matern_plan *plan, const double *l
 int bgk_ipc_export(const void *ptr, void *handle, uint64_t *offset);
 int bgk_ipc_open(const void *handle, uint64_t offset, void **ptr);
 int bgk_ipc_close(void *ptr, uint64_t offset);
+/* *can_access = cudaDeviceCanAccessPeer(current device, peer) (1 for the same device):
+ * checked before any peer mapping. */
+int bgk_can_access_peer(int peer_device, int *can_access);
 /* cudaDeviceEnablePeerAccess(peer) on the current device; already-enabled is OK. */
 int bgk_enable_peer_access(int peer_device);
 

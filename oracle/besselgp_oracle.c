@@ -429,11 +429,66 @@ static void *cov_worker(void *arg) {
  * produces the full N x N matrix (row0=0,row1=N).  mirror=0 produces the row
  * block [row0,row1) by computing every tile of those rows directly (used to
  * time a bounded sample of the big configs). */
+static void generate_covariance_impl(const double *lx, const double *ly, int64_t N,
+                                     double sigma_sq, double beta, double nu, double t0,
+                                     double t1, int64_t bins, double thr, double eps,
+                                     int64_t series_cap, int64_t tile_size, int64_t row0,
+                                     int64_t row1, int mirror, double *out, int64_t ld,
+                                     int threads, int64_t l0, int64_t l1);
+
 void orc_generate_covariance(const double *lx, const double *ly, int64_t N, double sigma_sq,
                              double beta, double nu, double t0, double t1, int64_t bins,
                              double thr, double eps, int64_t series_cap, int64_t tile_size,
                              int64_t row0, int64_t row1, int mirror, double *out, int64_t ld,
                              int threads) {
+  generate_covariance_impl(lx, ly, N, sigma_sq, beta, nu, t0, t1, bins, thr, eps, series_cap,
+                           tile_size, row0, row1, mirror, out, ld, threads, 0, -1);
+}
+
+/* The full-matrix job (lower tiles + mirror) restricted to lower-tile indices
+ * [l0, l1): K calls over a partition of [0, T(T+1)/2) produce the whole matrix,
+ * so bench.py can spread one generate_covariance over K timed steps. */
+void orc_generate_covariance_tiles(const double *lx, const double *ly, int64_t N,
+                                   double sigma_sq, double beta, double nu, double t0, double t1,
+                                   int64_t bins, double thr, double eps, int64_t series_cap,
+                                   int64_t tile_size, int64_t l0, int64_t l1, double *out,
+                                   int64_t ld, int threads) {
+  generate_covariance_impl(lx, ly, N, sigma_sq, beta, nu, t0, t1, bins, thr, eps, series_cap,
+                           tile_size, 0, N, 1, out, ld, threads, l0, l1);
+}
+
+/* First touch of a host buffer with `threads` threads (page faults outside a timed
+ * region). */
+typedef struct {
+  double *p;
+  int64_t n;
+  int t, nt;
+} touch_job;
+static void *touch_worker(void *arg) {
+  touch_job *J = (touch_job *)arg;
+  int64_t a = J->n * J->t / J->nt, b = J->n * (J->t + 1) / J->nt;
+  memset(J->p + a, 0, sizeof(double) * (size_t)(b - a));
+  return NULL;
+}
+void orc_touch(double *p, int64_t n, int threads) {
+  if (threads < 1) threads = 1;
+  pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)threads);
+  touch_job *jobs = (touch_job *)malloc(sizeof(touch_job) * (size_t)threads);
+  for (int t = 0; t < threads; ++t) {
+    jobs[t].p = p; jobs[t].n = n; jobs[t].t = t; jobs[t].nt = threads;
+    pthread_create(&th[t], NULL, touch_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+  free(jobs);
+  free(th);
+}
+
+static void generate_covariance_impl(const double *lx, const double *ly, int64_t N,
+                                     double sigma_sq, double beta, double nu, double t0,
+                                     double t1, int64_t bins, double thr, double eps,
+                                     int64_t series_cap, int64_t tile_size, int64_t row0,
+                                     int64_t row1, int mirror, double *out, int64_t ld,
+                                     int threads, int64_t l0, int64_t l1) {
   cov_job J;
   double *c = (double *)malloc(sizeof(double) * (size_t)(bins + 1));
   double *a = (double *)malloc(sizeof(double) * (size_t)(bins + 1));
@@ -461,6 +516,8 @@ void orc_generate_covariance(const double *lx, const double *ly, int64_t N, doub
   J.next = 0;
   if (mirror) {
     J.ntiles = J.T * (J.T + 1) / 2;
+    if (l1 >= 0 && l1 < J.ntiles) J.ntiles = l1;
+    J.next = l0 > 0 ? l0 : 0;
   } else {
     int64_t p0 = J.row0 / tile_size, p1 = (J.row1 + tile_size - 1) / tile_size;
     J.ntiles = (p1 - p0) * J.T;

@@ -95,6 +95,8 @@ _int = ctypes.c_int
 # symbol -> (restype, argtypes); kept in sync with include/besselgp_b200.h
 SIGNATURES = {
     "bgk_besselk_batch": (_int, [_vp, _vp, _i64, ctypes.POINTER(BgkConfig), _int, _vp, _vp, _vp, _vp]),
+    "bgk_besselk_scalar": (_int, [_d, _d, ctypes.POINTER(BgkConfig), _int,
+                                  ctypes.POINTER(ctypes.c_double), _vp]),
     "bgk_besselk_windows_host": (_int, [_vp, _vp, _i64, ctypes.POINTER(BgkConfig), _vp, _vp, _vp]),
     "bgk_besselk_windows": (_int, [_vp, _vp, _i64, ctypes.POINTER(BgkConfig), _vp, _vp, _vp, _vp]),
     "bgk_temme_sums_batch": (_int, [_vp, _vp, _i64, ctypes.POINTER(BgkConfig), _vp, _vp, _vp, _vp]),
@@ -129,6 +131,7 @@ SIGNATURES = {
     "bgk_ipc_open": (_int, [_vp, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]),
     "bgk_ipc_close": (_int, [_vp, ctypes.c_uint64]),
     "bgk_enable_peer_access": (_int, [_int]),
+    "bgk_can_access_peer": (_int, [_int, ctypes.POINTER(ctypes.c_int)]),
     "bgk_normalize_locations": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "bgk_morton_keys": (_int, [_vp, _vp, _i64, _int, _vp, _vp]),
     "bgk_log_grid": (_int, [_vp, _i64, _vp, _i64, ctypes.POINTER(BgkConfig), _int, _i64, _int, _vp,
@@ -167,13 +170,20 @@ def load_library():
     return _lib
 
 
+_cuda_ok = False
+
+
 def lib():
     """The bound library, after checking a CUDA device is present."""
+    global _cuda_ok
+    if _cuda_ok:
+        return _lib
     import torch
 
     L = load_library()
     if not torch.cuda.is_available():
         raise BackendUnavailable("no CUDA device visible: the sm_100a kernels are the only backend")
+    _cuda_ok = True
     return L
 
 

@@ -345,13 +345,22 @@ def _host_pipeline_locked(torch, dev, xf, nf, n, shape, cfg, route, validate):
                        out_p.numpy().reshape(shape))
 
 
+_CFG_C: dict = {}  # (cfg, bins) -> bgk_config, built once
+
+
 def _scalar_logk(x: float, nu: float, cfg: QuadratureConfig, route: int,
                  bins: int | None = None) -> float:
-    xd = _to_device([x])
-    nud = _to_device([nu], xd.device)
-    logk, _, _ = _launch_besselk(xd, nud, cfg, route, want_value=False, want_path=False,
-                                 bins=bins)
-    return float(logk.cpu()[0])
+    """One evaluation on the current device: bgk_besselk_scalar (inputs and result
+    through a mapped page-locked slot, one launch + one sync, no torch tensors)."""
+    L = _lib.lib()
+    key = (cfg, bins)
+    c = _CFG_C.get(key)
+    if c is None:
+        c = _CFG_C.setdefault(key, cfg.to_c(bins))
+    out = ctypes.c_double()
+    _lib.check(L.bgk_besselk_scalar(float(x), float(nu), ctypes.byref(c), route,
+                                    ctypes.byref(out), _stream_handle()), "bgk_besselk_scalar")
+    return out.value
 
 
 # ---------------------------------------------------------------------------------------

@@ -714,6 +714,54 @@ extern "C" int bgk_besselk_windows(const double *x, const double *nu, int64_t n,
   return bgk_check_launch("bk_windows_kernel");
 }
 
+// One (x, nu) through the batch kernel with no copies: the inputs and the result
+// live in a per-(thread, device) page-locked, device-mapped host slot that the
+// kernel reads and writes over PCIe, so a call costs one launch and one stream
+// sync (the scalar drop-in API, besselk.py:94-165).  Bitwise the batch result.
+extern "C" int bgk_besselk_scalar(double x, double nu, const bgk_config *cfg, int route,
+                                  double *log_k, void *stream) {
+  if (!cfg || !log_k || route < 0 || route > 2 || cfg->bins < 1 ||
+      !(cfg->t_upper > cfg->t_lower)) {
+    bgk_set_error("bgk_besselk_scalar: bad arguments");
+    return BGK_ERR_INVALID;
+  }
+  struct Slot {
+    int key;
+    double *host;  // [x, nu, log_k]
+    double *dev;   // the same memory, device view
+  };
+  thread_local std::vector<Slot> slots;
+  const int key = bgk_device_key(nullptr);
+  Slot *sl = nullptr;
+  for (Slot &e : slots)
+    if (e.key == key) sl = &e;
+  if (!sl) {
+    Slot e{key, nullptr, nullptr};
+    cudaError_t err = cudaHostAlloc((void **)&e.host, 4 * sizeof(double), cudaHostAllocMapped);
+    if (err == cudaSuccess) err = cudaHostGetDevicePointer((void **)&e.dev, e.host, 0);
+    if (err != cudaSuccess) {
+      cudaGetLastError();
+      bgk_set_error("bgk_besselk_scalar: mapped host slot: %s", cudaGetErrorString(err));
+      return BGK_ERR_CUDA;
+    }
+    slots.push_back(e);
+    sl = &slots.back();
+  }
+  volatile double *h = sl->host;
+  h[0] = x;
+  h[1] = nu;
+  if (int rc = bgk_launch_besselk(sl->dev, sl->dev + 1, 1, cfg, route, sl->dev + 2, nullptr,
+                                  nullptr, (cudaStream_t)stream))
+    return rc;
+  const cudaError_t err = cudaStreamSynchronize((cudaStream_t)stream);
+  if (err != cudaSuccess) {
+    bgk_set_error("bgk_besselk_scalar: %s", cudaGetErrorString(err));
+    return BGK_ERR_CUDA;
+  }
+  *log_k = h[2];
+  return BGK_OK;
+}
+
 int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_config *cfg,
                        int route, double *log_k, double *k, uint8_t *path, cudaStream_t stream) {
   if (n == 0) return 0;

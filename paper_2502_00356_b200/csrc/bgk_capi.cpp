@@ -639,6 +639,26 @@ int bgk_ipc_close(void *ptr, uint64_t offset) {
   return BGK_OK;
 }
 
+int bgk_can_access_peer(int peer_device, int *can_access) {
+  int dev = 0;
+  if (!can_access) {
+    bgk_set_error("bgk_can_access_peer: NULL result pointer");
+    return BGK_ERR_INVALID;
+  }
+  cudaGetDevice(&dev);
+  if (peer_device == dev) {
+    *can_access = 1;
+    return BGK_OK;
+  }
+  const cudaError_t e = cudaDeviceCanAccessPeer(can_access, dev, peer_device);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    bgk_set_error("cudaDeviceCanAccessPeer(%d, %d): %s", dev, peer_device, cudaGetErrorString(e));
+    return BGK_ERR_CUDA;
+  }
+  return BGK_OK;
+}
+
 int bgk_enable_peer_access(int peer_device) {
   cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
   if (e == cudaErrorPeerAccessAlreadyEnabled) {

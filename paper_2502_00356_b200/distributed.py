@@ -310,16 +310,34 @@ class PeerMatrix:
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine, group=group)
         self.bases, self._opened = [], []
-        for h, (hb, o, dev, ok) in enumerate(everyone):
-            if h == self.rank or not ok:
-                self.bases.append(ptr or 1)  # empty blocks are never written
-                continue
-            if dev != self.device.index:
-                _lib.check(L.bgk_enable_peer_access(dev), "bgk_enable_peer_access")
-            p = ctypes.c_void_p()
-            _lib.check(L.bgk_ipc_open(hb, o, ctypes.byref(p)), "bgk_ipc_open")
-            self.bases.append(p.value)
-            self._opened.append((p.value, o))
+        err = None
+        try:
+            for h, (hb, o, dev, ok) in enumerate(everyone):
+                if h == self.rank or not ok:
+                    self.bases.append(ptr or 1)  # empty blocks are never written
+                    continue
+                if dev != self.device.index:
+                    can = ctypes.c_int(0)
+                    _lib.check(L.bgk_can_access_peer(dev, ctypes.byref(can)),
+                               "bgk_can_access_peer")
+                    if not can.value:
+                        raise RuntimeError(f"cudaDeviceCanAccessPeer({self.device.index} -> "
+                                           f"{dev}) = 0: no P2P path for the mirror stores")
+                    _lib.check(L.bgk_enable_peer_access(dev), "bgk_enable_peer_access")
+                p = ctypes.c_void_p()
+                _lib.check(L.bgk_ipc_open(hb, o, ctypes.byref(p)), "bgk_ipc_open")
+                self.bases.append(p.value)
+                self._opened.append((p.value, o))
+        except Exception as ex:  # noqa: BLE001 -- reported collectively below
+            err = f"rank {self.rank}: {type(ex).__name__}: {ex}"
+        # every rank learns whether every rank mapped every peer, so they all take the
+        # peer path or all fall back together (no rank left waiting in a collective)
+        errs = [None] * self.world
+        dist.all_gather_object(errs, err, group=group)
+        bad = [e for e in errs if e]
+        if bad:
+            self.close()
+            raise RuntimeError("peer mapping failed: " + "; ".join(bad))
         self.starts = macro_row_starts(N, self.world)
         if mode not in PEER_MODES:
             raise ValueError(f"mode must be one of {PEER_MODES}")
