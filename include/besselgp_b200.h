@@ -304,6 +304,12 @@ int bgk_host_copy(void *dst, const void *src, int64_t bytes, int nthreads);
  * __dsqrt_rn(x[i]).  Device pointers. */
 int bgk_sqrt_rn_check(const double *x, int64_t n, double *fast, double *ref, void *stream);
 
+/* Launch geometry of the Matern kernel for this plan on the current device (test /
+ * profiling hook): resident CTAs per SM, dynamic + static shared bytes per CTA,
+ * registers per thread.  Sets the kernel's shared-memory opt-in like a launch. */
+int bgk_matern_kernel_info(const bgk_matern_plan *plan, int *ctas_per_sm, int *smem_bytes,
+                           int *regs);
+
 /* Number of kernel launches issued by this library since load (for bench.py's
  * gpu_launches accounting). */
 int64_t bgk_launch_count(void);

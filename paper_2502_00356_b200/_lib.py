@@ -117,6 +117,8 @@ SIGNATURES = {
     "bgk_debug_set_device_alias": (_int, [_int]),
     "bgk_fp64_probe": (_int, [_vp, _i64, _int, _vp, ctypes.POINTER(ctypes.c_double)]),
     "bgk_sqrt_rn_check": (_int, [_vp, _i64, _vp, _vp, _vp]),
+    "bgk_matern_kernel_info": (_int, [ctypes.POINTER(BgkMaternPlan), ctypes.POINTER(ctypes.c_int),
+                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "bgk_matern_covariance_peer": (_int, [ctypes.POINTER(BgkMaternPlan), _vp, _vp, _i64, _int,
                                           ctypes.POINTER(ctypes.c_int64),
                                           ctypes.POINTER(ctypes.c_void_p), _i64, _i64, _vp]),

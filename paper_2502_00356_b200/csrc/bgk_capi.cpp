@@ -301,6 +301,15 @@ int bgk_ensure_smem_optin(const void *kernel, const char *name, int bytes) {
     bgk_set_error("cudaFuncSetAttribute(%s, %d bytes): %s", name, bytes, cudaGetErrorString(e));
     return BGK_ERR_CUDA;
   }
+  // the whole unified L1/shared array as shared memory: the kernels are sized for
+  // several ~55 KB CTAs per SM and use no L1-cached global data worth keeping
+  const cudaError_t e2 = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                              (int)cudaSharedmemCarveoutMaxShared);
+  if (e2 != cudaSuccess) {
+    cudaGetLastError();
+    bgk_set_error("cudaFuncSetAttribute(%s, carveout): %s", name, cudaGetErrorString(e2));
+    return BGK_ERR_CUDA;
+  }
   for (OptIn &o : g_optins)
     if (o.kernel == kernel && o.dev == key) {
       o.bytes = bytes;

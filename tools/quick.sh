@@ -3,7 +3,7 @@
 # CPU legs) and one ncu --set full capture of the kernel.  usage: bash tools/quick.sh TAG [--bk]
 TAG=${1:-q}; shift
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_parity_matern.py tests/test_parity_edges.py tests/test_full_size.py tests/test_api_gpu.py tests/test_preprocess_gp.py tests/test_peer.py -m gpu -x -q > gpurun_out/quick_pytest_$TAG.log 2>&1
+timeout 900 python -m pytest tests/test_parity_matern.py tests/test_parity_edges.py tests/test_full_size.py tests/test_api_gpu.py tests/test_preprocess_gp.py tests/test_peer.py tests/test_kernel_geometry.py -m gpu -x -q > gpurun_out/quick_pytest_$TAG.log 2>&1
 echo "pytest rc=$? $(tail -1 gpurun_out/quick_pytest_$TAG.log)"
 for w in m100 m50; do
   timeout 600 python bench.py --workload $w --no-e2e --no-cpu-baseline --no-secondary --steps 5 > gpurun_out/quick_${w}_$TAG.json 2> gpurun_out/quick_${w}_$TAG.err
