@@ -310,6 +310,13 @@ int bgk_sqrt_rn_check(const double *x, int64_t n, double *fast, double *ref, voi
 int bgk_matern_kernel_info(const bgk_matern_plan *plan, int *ctas_per_sm, int *smem_bytes,
                            int *regs);
 
+/* Profiling hook: per-barrier work / wait cycles of the Matern kernel's task loop
+ * summed over all warps since the last reset (12 values: work, wait for the
+ * barriers after classify, in the scan, after the scan, after the scatter, after
+ * the compute phase, after the stores).  Only libraries built with
+ * -DBGK_MATERN_PROFILE=1 (tools/matern_phases.py); else BGK_ERR_UNSUPPORTED. */
+int bgk_matern_phase_profile(double *out12, int reset);
+
 /* Number of kernel launches issued by this library since load (for bench.py's
  * gpu_launches accounting). */
 int64_t bgk_launch_count(void);

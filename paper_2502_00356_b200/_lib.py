@@ -117,6 +117,7 @@ SIGNATURES = {
     "bgk_debug_set_device_alias": (_int, [_int]),
     "bgk_fp64_probe": (_int, [_vp, _i64, _int, _vp, ctypes.POINTER(ctypes.c_double)]),
     "bgk_sqrt_rn_check": (_int, [_vp, _i64, _vp, _vp, _vp]),
+    "bgk_matern_phase_profile": (_int, [_vp, _int]),
     "bgk_matern_kernel_info": (_int, [ctypes.POINTER(BgkMaternPlan), ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "bgk_matern_covariance_peer": (_int, [ctypes.POINTER(BgkMaternPlan), _vp, _vp, _i64, _int,
@@ -150,6 +151,11 @@ def build(force: bool = False) -> str:
     return LIB_PATH
 
 
+# test / profiling hooks, not compute entry points: tolerated missing so that
+# tools/ab_libs.sh can time libraries built from older revisions
+_INTROSPECTION = {"bgk_matern_kernel_info", "bgk_matern_phase_profile"}
+
+
 def load_library():
     """Load the shared object and bind every exported symbol (no device needed)."""
     global _lib
@@ -161,6 +167,8 @@ def load_library():
                     "(there is no CPU fallback)")
             lib = ctypes.CDLL(LIB_PATH)
             for name, (res, args) in SIGNATURES.items():
+                if name in _INTROSPECTION and not hasattr(lib, name):
+                    continue  # profiling hooks only (an older library in an A/B run)
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
