@@ -425,6 +425,46 @@ __global__ void __launch_bounds__(kBkThreads, BGK_BK_MINBLOCKS) besselk_kernel(c
   }
 }
 
+// One (x, nu) on one warp: the batch kernel's per-element path without the chunk
+// staging and the sort (the scalar drop-in API, besselk.py:94-165).  The same
+// device routines on the same inputs -- fixed_window_fast is warp-collective, lane
+// 0 active -- so the value is bitwise the batch kernel's.  x and nu arrive as
+// kernel parameters; log K and then the call's sequence number are written to a
+// page-locked, device-mapped host slot that the host polls.
+__global__ void __launch_bounds__(32) besselk_scalar_kernel(const __grid_constant__ BkArgs A,
+                                                            double x, double nu, double *slot,
+                                                            unsigned long long seq) {
+  extern __shared__ __align__(16) unsigned char bk_smem[];
+  __shared__ double s_exp[128], s_invc[128], s_logc[128];
+  double2 *cw = reinterpret_cast<double2 *>(bk_smem);
+  const int lane = threadIdx.x;
+  const int ncw = A.table_ok ? A.bins + 1 : 0;
+  load_tables128(s_exp, s_invc, s_logc);
+  for (int k = lane; k < ncw; k += 32) cw[k] = __ldg(A.cwg + k);
+  __syncwarp();
+  const double a = fabs(nu);
+  const bool series = (A.route == 1) || (A.route == 0 && x < A.thr);
+  uint32_t w = 0;
+  if (!series) {
+    const double tmax = fmax(fabs(A.t0), fabs(A.t1));
+    const double cmax = ncw ? cw[A.bins].x : 0.0;
+    w = bk_window_word(x, a, A.table_ok, tmax, cmax, A.bins, A.win);
+  }
+  const bool fast = lane == 0 && w != 0u;
+  double lk = fixed_window_fast(fast, x, a, w, A, cw, s_exp, s_invc, s_logc);
+  if (lane == 0) {
+    if (series) {
+      lk = bk_series_log(x, nu, A.eps, A.cap);
+    } else if (!fast) {
+      lk = fixed_window_log_ref(x, nu, A.t0, A.t1, A.bins);
+    }
+    volatile double *v = slot;
+    v[0] = lk;
+    __threadfence_system();  // the value is visible to the host before the sequence number
+    reinterpret_cast<volatile unsigned long long *>(slot)[1] = seq;
+  }
+}
+
 __global__ void temme_sums_kernel(const double *x, const double *mu, long long n, double eps,
                                   long long cap, double *s0, double *s1, int64_t *terms) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -714,10 +754,12 @@ extern "C" int bgk_besselk_windows(const double *x, const double *nu, int64_t n,
   return bgk_check_launch("bk_windows_kernel");
 }
 
-// One (x, nu) through the batch kernel with no copies: the inputs and the result
-// live in a per-(thread, device) page-locked, device-mapped host slot that the
-// kernel reads and writes over PCIe, so a call costs one launch and one stream
-// sync (the scalar drop-in API, besselk.py:94-165).  Bitwise the batch result.
+// One (x, nu): besselk_scalar_kernel on one warp, the inputs as kernel parameters,
+// the result through a per-(thread, device) page-locked, device-mapped host slot
+// [log K, sequence number] that the host polls -- no copies and no stream
+// synchronisation on the fast path (the scalar drop-in API, besselk.py:94-165).
+// Bitwise the batch result.  The poll falls back to cudaStreamQuery every 4096 spins,
+// so a launch or kernel fault is reported instead of spinning forever.
 extern "C" int bgk_besselk_scalar(double x, double nu, const bgk_config *cfg, int route,
                                   double *log_k, void *stream) {
   if (!cfg || !log_k || route < 0 || route > 2 || cfg->bins < 1 ||
@@ -727,8 +769,9 @@ extern "C" int bgk_besselk_scalar(double x, double nu, const bgk_config *cfg, in
   }
   struct Slot {
     int key;
-    double *host;  // [x, nu, log_k]
+    double *host;  // [log_k, seq]
     double *dev;   // the same memory, device view
+    unsigned long long seq;
   };
   thread_local std::vector<Slot> slots;
   const int key = bgk_device_key(nullptr);
@@ -736,7 +779,7 @@ extern "C" int bgk_besselk_scalar(double x, double nu, const bgk_config *cfg, in
   for (Slot &e : slots)
     if (e.key == key) sl = &e;
   if (!sl) {
-    Slot e{key, nullptr, nullptr};
+    Slot e{key, nullptr, nullptr, 0};
     cudaError_t err = cudaHostAlloc((void **)&e.host, 4 * sizeof(double), cudaHostAllocMapped);
     if (err == cudaSuccess) err = cudaHostGetDevicePointer((void **)&e.dev, e.host, 0);
     if (err != cudaSuccess) {
@@ -744,21 +787,38 @@ extern "C" int bgk_besselk_scalar(double x, double nu, const bgk_config *cfg, in
       bgk_set_error("bgk_besselk_scalar: mapped host slot: %s", cudaGetErrorString(err));
       return BGK_ERR_CUDA;
     }
+    reinterpret_cast<volatile unsigned long long *>(e.host)[1] = 0;
     slots.push_back(e);
     sl = &slots.back();
   }
-  volatile double *h = sl->host;
-  h[0] = x;
-  h[1] = nu;
-  if (int rc = bgk_launch_besselk(sl->dev, sl->dev + 1, 1, cfg, route, sl->dev + 2, nullptr,
-                                  nullptr, (cudaStream_t)stream))
+  bgk::BkArgs A;
+  bk_fill_args(A, nullptr, nullptr, 1, cfg, route, nullptr, nullptr, nullptr);
+  if (int rc = bk_device_tables(cfg, A)) return rc;
+  const size_t smem = A.table_ok ? sizeof(double2) * ((size_t)cfg->bins + 1) : 0;
+  if (int rc = bgk_ensure_smem_optin((const void *)bgk::besselk_scalar_kernel,
+                                     "besselk_scalar_kernel",
+                                     (int)(sizeof(double2) * (kMaxTable + 1))))
     return rc;
-  const cudaError_t err = cudaStreamSynchronize((cudaStream_t)stream);
-  if (err != cudaSuccess) {
-    bgk_set_error("bgk_besselk_scalar: %s", cudaGetErrorString(err));
-    return BGK_ERR_CUDA;
+  const unsigned long long seq = ++sl->seq;
+  bgk::besselk_scalar_kernel<<<1, 32, smem, (cudaStream_t)stream>>>(A, x, nu, sl->dev, seq);
+  bgk_note_launch();
+  if (int rc = bgk_check_launch("besselk_scalar_kernel")) return rc;
+  volatile unsigned long long *flag = reinterpret_cast<volatile unsigned long long *>(sl->host) + 1;
+  for (unsigned spins = 1; *flag != seq; ++spins) {
+    if ((spins & 4095) == 0) {
+      const cudaError_t q = cudaStreamQuery((cudaStream_t)stream);
+      if (q == cudaSuccess && *flag == seq) break;
+      if (q != cudaSuccess && q != cudaErrorNotReady) {
+        bgk_set_error("bgk_besselk_scalar: %s", cudaGetErrorString(q));
+        return BGK_ERR_CUDA;
+      }
+      if (q == cudaSuccess && *flag != seq) {
+        bgk_set_error("bgk_besselk_scalar: kernel finished without a result");
+        return BGK_ERR_CUDA;
+      }
+    }
   }
-  *log_k = h[2];
+  *log_k = reinterpret_cast<volatile double *>(sl->host)[0];
   return BGK_OK;
 }
 
