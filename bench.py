@@ -112,6 +112,16 @@ class Dist:
         if torch.cuda.is_available():
             self.device_index = self.local % torch.cuda.device_count()
             torch.cuda.set_device(self.device_index)
+            # NCCL refuses two ranks on one GPU: when the node has fewer GPUs than
+            # local ranks (a harness test on a one-GPU box), the control-plane
+            # collectives (barrier, max over ranks) go over gloo instead -- the data
+            # path has no collective either way
+            lws = int(os.environ.get("LOCAL_WORLD_SIZE", str(self.world)))
+            if (self.backend == "nccl" and "BGK_BENCH_BACKEND" not in os.environ
+                    and torch.cuda.device_count() < lws):
+                self.backend = "gloo"
+                log(f"[bench] {lws} local ranks on {torch.cuda.device_count()} GPU(s): "
+                    "gloo for barriers and reductions")
         if self.world > 1 and self.pg is None:
             import torch.distributed as dist
 
@@ -865,6 +875,8 @@ def main():
     nccl = D.nccl_summary() if D.rank == 0 else None
     if D.rank == 0:
         line = build_line(args, D.world, wl, matern, r, sec, peaks, fp64, pcie, scalar, nccl)
+        if D.world > 1:
+            line["control_backend"] = D.backend  # barriers / max over ranks (no data-path collective)
         print(json.dumps(line), flush=True)
     D.barrier()
     D.close()
