@@ -191,7 +191,7 @@ def bessel_k_batch(x, nu, cfg: QuadratureConfig = DEFAULT_CONFIG, route: str = "
     if not on_device and not isinstance(nu, torch.Tensor):
         xa = np.asarray(x, dtype=np.float64)
         na = np.asarray(nu, dtype=np.float64)
-        if xa.shape == na.shape and xa.size >= _HOST_CHUNK:
+        if xa.shape == na.shape and xa.size >= _HOST_PIPELINE_MIN:
             return _bessel_k_host_pipelined(xa, na, cfg, route, validate)
     xd = _to_device(x)
     nud = _to_device(nu, xd.device)
@@ -233,6 +233,9 @@ def _validate_batch(xd, nud, cfg, route):
 
 
 _HOST_CHUNK = 1 << 22  # elements per pipelined chunk for host (numpy) batches
+# host batches from this size on take the pinned-staging path even as one chunk (1M
+# elements on B200: 4.4 ms vs 6.0 ms through pageable copies; tools/bk_small_e2e.py)
+_HOST_PIPELINE_MIN = 1 << 16
 
 
 _STAGE: dict = {}  # per device: two pinned staging slots (x, nu) of _HOST_CHUNK elements
