@@ -78,10 +78,12 @@ int bgk_besselk_batch(const double *x, const double *nu, int64_t n, const bgk_co
 /* Temme starting sums (s0, s1, terms) with K_mu = s0, K_{mu+1} = (2/x) s1.
  * Replaces kernels.temme_sums (kernels.py:230-270) as called by
  * besselk.temme_pair (besselk.py:94-101).  terms may be NULL. */
-/* One (x, nu): ln K into *log_k (a HOST pointer), synchronously on `stream`.  The
- * inputs and result travel through a per-thread, per-device mapped page-locked
- * slot (no memcpy calls): one kernel launch + one stream sync.  Same bits as
- * bgk_besselk_batch.  Backs the scalar drop-in API (besselk.py:94-165). */
+/* One (x, nu): ln K into *log_k (a HOST pointer), synchronously on `stream`.  One
+ * one-warp kernel launch with x and nu as kernel parameters; the result and a
+ * sequence number come back through a per-thread, per-device mapped page-locked
+ * slot that the host polls (no memcpy, no stream sync; a fault is still reported
+ * through periodic cudaStreamQuery).  Same bits as bgk_besselk_batch.  Backs the
+ * scalar drop-in API (besselk.py:94-165). */
 int bgk_besselk_scalar(double x, double nu, const bgk_config *cfg, int route, double *log_k,
                        void *stream);
 
