@@ -68,6 +68,9 @@ constexpr int kBkChunkBytes = kBkChunk * (8 + 8 + 4 + 2 + 1 + 1);  // + 1: keeps
 #ifndef BGK_BK_NODE_I2F
 #define BGK_BK_NODE_I2F 0  // A/B on B200: 1 -> 1.521 vs 0 -> 1.511 ms (the Matern loop gains, this one not)
 #endif
+#ifndef BGK_BK_NODE_IMM
+#define BGK_BK_NODE_IMM 1  // 1/24 (20-bit mantissa) and the magic as immediates: 1.503 -> 1.499 ms (BK 64 Mi)
+#endif
 #ifndef BGK_BK_NODE_UNROLL
 #define BGK_BK_NODE_UNROLL 2
 #endif
@@ -253,10 +256,20 @@ __device__ __forceinline__ double fixed_window_fast(bool active, double x, doubl
 #if BGK_BK_NODE_I2F
     const double nd = __int2double_rn(nn);  // conversion pipe, exact (= tt - magic)
 #else
+#if BGK_BK_NODE_IMM
+    const double nd = tt - 0x1.8p52;  // (the magic as a DADD immediate)
+#else
     const double nd = tt - kExpK[6];
 #endif
+#endif
     const double r = fma(nd, -kExpK[1], y);
+#if BGK_BK_NODE_IMM
+    // 1/24 rounded to a 20-bit mantissa (a DFMA immediate; |r| <= ln2/256: the change
+    // is < 1e-18 of the term), so this step reads one vector register, not two
+    double q = fma(r, 0x1.55555p-5, kExpK[4]);
+#else
     double q = fma(r, kExpK[3], kExpK[4]);
+#endif
     q = fma(q, r, 0.5);
     q = fma(q, r, 1.0);
     const double p = fma(q, r, 1.0);
