@@ -51,6 +51,29 @@ def test_m100_full_matrix(oracle):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("nu", [0.3, 0.8, 1.7, 2.9])
+def test_m50_full_matrix_nu_sweep(oracle, nu):
+    """BASELINE's M50 configuration at its full size (N=50K, 20 GB per matrix, the
+    non-half-integer orders take the exp(nu ln u) epilogue): whole sampled rows vs the
+    oracle, exact symmetry of those rows / columns, exact sigma^2 diagonal."""
+    import paper_2502_00356_b200 as bg
+
+    N = 50_000
+    locs = np.random.default_rng(SEED).random((N, 2))
+    out = bg.generate_covariance(locs, bg.MaternParams(1.0, 0.1, nu), device="cuda").data
+    rng = np.random.default_rng(int(nu * 10))
+    rows = np.unique(np.concatenate([[0, 63, 64, N - 1], rng.integers(0, N, 6)]))
+    got = out[torch.from_numpy(rows).cuda()].cpu().numpy()
+    ref = oracle.matern_entries(locs[rows, 0], locs[rows, 1], locs[:, 0], locs[:, 1], 1.0, 0.1, nu)
+    err = _rel(got, ref)
+    assert err.max() <= TOL, err.max()
+    cols = out[:, torch.from_numpy(rows).cuda()].T.cpu().numpy()
+    assert np.array_equal(cols, got)
+    assert bool((torch.diagonal(out) == 1.0).all())
+    del out
+    torch.cuda.empty_cache()
+
+
 def test_bk_full_batch(oracle):
     import paper_2502_00356_b200 as bg
 
