@@ -650,7 +650,7 @@ def run_matern(args, D: Dist) -> dict:
             res["e2e_how"] = (
                 "paper_2502_00356_b200.generate_covariance(numpy locs, theta, out=pinned host "
                 "array): H2D of the locations; per 1 GB row block the device computes the lower "
-                f"part, a 2D copy moves it (half the matrix over PCIe) and {max(1, _host_threads() // 2)} "
+                f"part, a 2D copy moves it (half the matrix over PCIe) and {max(1, _host_threads() * 3 // 4)} "
                 "host threads mirror it into the upper triangle (non-temporal stores) while the "
                 "next block computes and copies; wall clock")
         else:

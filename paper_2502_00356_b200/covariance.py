@@ -609,10 +609,10 @@ def _full_host_lower_mirrored(plan, lx, ly, N, host, block_bytes):
         from concurrent.futures import ThreadPoolExecutor
 
         _MIRROR_POOL = ThreadPoolExecutor(max_workers=1)  # mirrors in block order
-    # half the host threads: the mirror then keeps pace with the copies and leaves
-    # DRAM bandwidth to the DMA (M100 on the 16-core box: 8 -> 1.04-1.06 s,
-    # 16 -> 1.07 s, 4 -> 1.4 s; tools/mirror_threads.py)
-    nthreads = _MIRROR_THREADS or max(1, _host_threads() // 2)
+    # 3/4 of the host threads: the mirror then keeps pace with the copies and leaves
+    # DRAM bandwidth to the DMA (M100 on a 16-core box, tools/e2e_sweep.py, median of
+    # 3 with 1 GiB blocks: 8 -> 0.890 s, 12 -> 0.820 s, 16 -> 0.894 s; round 1: 4 -> 1.4 s)
+    nthreads = _MIRROR_THREADS or max(1, _host_threads() * 3 // 4)
     block = max(64, min(N, (block_bytes // (8 * N)) // 64 * 64))
     w = _mirror_direct_blocks(N, block)
     dev = lx.device
