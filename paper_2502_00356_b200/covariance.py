@@ -550,7 +550,8 @@ def generate_covariance(locs, theta: MaternParams, cfg: QuadratureConfig = DEFAU
 _MIRROR_MIN_N = 4096
 _MIRROR_POOL = None
 _MIRROR_DIRECT = None  # override of _mirror_direct_blocks (tests / tuning)
-_MIRROR_THREADS = None  # host threads of the mirror (default: all)
+_MIRROR_THREADS = None  # host threads of the mirror (default: 3/4)
+_MIRROR_REVERSE = True  # row blocks bottom-up (A/B: 0.800-0.818 vs 0.813-0.832 s, tools/e2e_reverse_check.py)
 
 
 def _is_pinned(a: np.ndarray) -> bool:
@@ -629,8 +630,15 @@ def _full_host_lower_mirrored(plan, lx, ly, N, host, block_bytes):
         _lib.check(L.bgk_host_mirror_block(hp, N, b0, b1, 0, max(0, b0 - w * block), nthreads),
                    "bgk_host_mirror_block")
 
+    # largest blocks first (the mirror of the last block is the one left uncovered at
+    # the end: make it the smallest).  Safe in either order: block k's copy writes
+    # rows [b0, b1) x cols [0, b1), its mirror rows [0, b0) x cols [b0, b1) -- no
+    # block's copy touches another block's mirror columns.
+    order = list(range(0, N, block))
+    if _MIRROR_REVERSE and w == 0:
+        order.reverse()
     try:
-        for bi, b0 in enumerate(range(0, N, block)):
+        for bi, b0 in enumerate(order):
             b1 = min(N, b0 + block)
             s = bi % 2
             if copied[s] is not None:
