@@ -1,6 +1,6 @@
 """M100 end to end (generate_covariance into a page-locked host array) over the host
 pipeline's knobs: mirror threads and row-block size (GPU box).
-usage: python tools/e2e_sweep.py"""
+usage: python tools/e2e_sweep.py [threads [block_MiB ...]]"""
 import os
 import sys
 import time
@@ -33,8 +33,8 @@ def run(threads, block):
 
 
 run(None, 1 << 30)  # warm-up
-for threads in (ncpu // 2, ncpu * 3 // 4, ncpu):
-    for block in (1 << 29, 1 << 30, 1 << 31):
+for threads in ([int(a) for a in sys.argv[1:2]] or [ncpu // 2, ncpu * 3 // 4, ncpu]):
+    for block in ([int(b) << 20 for b in sys.argv[2:]] or [1 << 29, 1 << 30, 1 << 31]):
         ts = run(threads, block)
         print(f"threads {threads:3d} block {block >> 20:5d} MiB: "
               + " ".join(f"{t:.3f}" for t in ts) + f"  median {sorted(ts)[1]:.3f} s", flush=True)
