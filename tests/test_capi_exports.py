@@ -58,6 +58,13 @@ def test_argument_validation_without_gpu(L):
     assert b"invalid bgk_config" in L.bgk_last_error()
     assert L.bgk_besselk_batch(None, None, 0, ctypes.byref(cfg), 7, None, None, None, None) == -1
     assert L.bgk_log_integrand_batch(None, None, None, 1, 3, None, None) == -1
+    # the scalar entry point: config, route and result pointer checked first
+    out = ctypes.c_double()
+    assert L.bgk_besselk_scalar(1.0, 1.5, None, 0, ctypes.byref(out), None) == -1
+    assert L.bgk_besselk_scalar(1.0, 1.5, ctypes.byref(cfg), 3, ctypes.byref(out), None) == -1
+    assert L.bgk_besselk_scalar(1.0, 1.5, ctypes.byref(bad_cfg), 0, ctypes.byref(out), None) == -1
+    assert L.bgk_besselk_scalar(1.0, 1.5, ctypes.byref(cfg), 0, None, None) == -1
+    assert b"bgk_besselk_scalar" in L.bgk_last_error()
     plan = _lib.BgkMaternPlan()
     assert L.bgk_matern_tile(ctypes.byref(plan), None, None, 1, None, None, 1, None, 1, 0, None) == -1
     assert b"uninitialised" in L.bgk_last_error()
