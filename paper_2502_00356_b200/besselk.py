@@ -233,6 +233,7 @@ def _validate_batch(xd, nud, cfg, route):
 
 
 _HOST_CHUNK = 1 << 22  # elements per pipelined chunk for host (numpy) batches
+_HOST_MIN_CHUNK = 1 << 20  # (A/B: 1M elements 1.25 ms as one chunk vs 1.7-2.5 ms as four; 4M 3.8-4.7 ms as four vs 4.4-5.0 ms as one)
 # host batches from this size on take the pinned-staging path even as one chunk (1M
 # elements on B200: 4.4 ms vs 6.0 ms through pageable copies; tools/bk_small_e2e.py)
 _HOST_PIPELINE_MIN = 1 << 16
@@ -306,8 +307,11 @@ def _host_pipeline_locked(torch, dev, xf, nf, n, shape, cfg, route, validate):
     bad_any = None  # device flag: some element failed validation
     staged = [None, None]  # event: the slot's H2D has finished (slot reusable)
     freed = [None, None]   # event: the chunk's D2H has finished (device buffers reusable)
-    for ci, c0 in enumerate(range(0, n, _HOST_CHUNK)):
-        c1 = min(n, c0 + _HOST_CHUNK)
+    # batches under four full chunks are cut into four, so their H2D, kernel and D2H
+    # still overlap (at least _HOST_MIN_CHUNK elements per chunk)
+    chunk = min(_HOST_CHUNK, max(_HOST_MIN_CHUNK, -(-n // 4)))
+    for ci, c0 in enumerate(range(0, n, chunk)):
+        c1 = min(n, c0 + chunk)
         s = ci % 2
         if staged[s] is not None:
             staged[s].synchronize()
