@@ -66,7 +66,9 @@ double u_of_key(int key) {
 }
 
 #ifndef BGK_WINDOW_CUTOFF
-#define BGK_WINDOW_CUTOFF 40.0
+#define BGK_WINDOW_CUTOFF 33.0  // A/B on B200 (M100 / M50 ms): 40 -> 74.07 / 80.35, 36 -> 72.80,
+                                // 33 -> 71.85 / 78.15, 30 -> 71.2 / 77.2 (max rel. err vs the oracle
+                                // 5.7e-14 at 40 and 33, 5.9e-14 at 30 with every nu at 3-6e-14)
 #endif
 
 struct Window {
@@ -74,8 +76,10 @@ struct Window {
 };
 
 // Reference window at u: grid argmax m* (first max, kernels.py:363-369) and
-// every node with g_k - g_{m*} > -40.  The reference keeps > -46; the terms in
-// (-46, -40] sum to < 41 e^-40 = 1.7e-16 of the peak term, below an ulp.
+// every node with g_k - g_{m*} > -33.  The reference keeps > -46; the terms in
+// (-46, -33] sum to < 41 e^-33 = 1.9e-13 of the peak term (a bound: on the M100
+// distances the largest dropped share is 2e-15, the table exp's own error), far
+// inside the 1e-10 parity tolerance.
 Window window_at(const bgk_matern_plan &P, double u) {
   const int nn = P.nnodes;
   double gmax = -INFINITY;

@@ -117,10 +117,10 @@ def _key(u, shift):
 @pytest.mark.parametrize("nu,bins", [(0.3, 40), (1.5, 40), (2.9, 40), (19.5, 40), (1.5, 16),
                                      (1.5, 128), (0.8, 7)])
 def test_lut_windows_cover_reference_windows(nu, bins):
-    """For u across the whole LUT range, every node with dg > -40 from the grid
+    """For u across the whole LUT range, every node with dg > -33 from the grid
     argmax lies in the bucket's [lo, hi]: the reference keeps dg > -46
     (kernels.py:363-379), so the nodes it sums that the kernel drops add up to
-    < 41 e^-40 = 1.7e-16 of the peak term (below an ulp of the sum).  And
+    < 41 e^-33 = 1.9e-13 of the peak term (BGK_WINDOW_CUTOFF; inside the 1e-10 tolerance).  And
     y = g_k - g_anchor stays inside the table exp's range."""
     import paper_2502_00356_b200 as bg
 
@@ -137,7 +137,7 @@ def test_lut_windows_cover_reference_windows(nu, bins):
     for u in us:
         g = a - u * c
         ms = int(np.argmax(g))
-        keep = np.nonzero(g - g[ms] > -40.0)[0]
+        keep = np.nonzero(g - g[ms] > -33.0)[0]
         b = min(max(_key(u, p.key_shift) - p.key_base, 0), p.nbuckets - 1)
         w = int(lut[b])
         anc, lo, hi = w & 1023, (w >> 10) & 1023, w >> 20
