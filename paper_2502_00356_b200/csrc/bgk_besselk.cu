@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -62,6 +63,7 @@ constexpr int kBkThreads = BGK_BK_THREADS;
 constexpr int kBkPerThread = BGK_BK_PER_THREAD;
 constexpr int kBkChunk = kBkThreads * kBkPerThread;
 constexpr int kBkChunkBytes = kBkChunk * (8 + 8 + 4 + 2 + 1 + 1);  // + 1: keeps cw 16-B aligned
+constexpr int bk_chunk_bytes(int per) { return kBkThreads * per * (8 + 8 + 4 + 2 + 1 + 1); }
 #ifndef BGK_BK_XBITS
 #define BGK_BK_XBITS 2  // window table: 2^XBITS x cells per octave
 #endif
@@ -299,7 +301,11 @@ __device__ __noinline__ double bk_series_log(double x, double nu, double eps, lo
   return temme_series_log_c(x, T, eps, cap);
 }
 
+// PER elements per thread (chunk = 256 PER): kBkPerThread, or fewer when that fills the
+// last wave of CTAs better (bgk_launch_besselk).
+template <int PER>
 __global__ void __launch_bounds__(kBkThreads, BGK_BK_MINBLOCKS) besselk_kernel(const __grid_constant__ BkArgs A) {
+  constexpr int kBkPerThread = PER, kBkChunk = kBkThreads * PER, kBkChunkBytes = bk_chunk_bytes(PER);
   extern __shared__ __align__(16) unsigned char bk_smem[];
   __shared__ double s_exp[128], s_invc[128], s_logc[128];
   __shared__ int hist[kBuckets + 1];
@@ -842,14 +848,50 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
   bgk::BkArgs A;
   bk_fill_args(A, x, nu, n, cfg, route, log_k, k, path);
   if (int rc = bk_device_tables(cfg, A)) return rc;
-  const size_t chunk_bytes = (size_t)bgk::kBkChunkBytes;
-  size_t smem = sizeof(double2) * (A.table_ok ? (size_t)cfg->bins + 1 : 0) + chunk_bytes;
-  // opt in once per device for the largest table (so every bins <= kMaxTable fits)
-  if (int rc = bgk_ensure_smem_optin((const void *)bgk::besselk_kernel, "besselk_kernel",
-                                     (int)(sizeof(double2) * (kMaxTable + 1) + chunk_bytes)))
-    return rc;
-  long long grid = (n + bgk::kBkChunk - 1) / bgk::kBkChunk;
-  bgk::besselk_kernel<<<(unsigned)grid, bgk::kBkThreads, smem, stream>>>(A);
+  // Elements per thread: 8 (2048 per CTA), or -- for batches of at most two waves of
+  // CTAs over the SMs x resident CTAs slots -- fewer when that evens out the last wave:
+  // cost ~ waves x chunk, ties to the larger chunk (1M elements: 586 CTAs of 1792 in
+  // one wave instead of 512 of 2048 on 592 slots, A/B on B200 40 -> 37 us).  Larger
+  // batches keep 2048: their CTAs finish at staggered times, so the waves do not
+  // quantise, and smaller chunks only add per-CTA set-up (64 Mi: 1.48 -> 1.58 ms).
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const long long slots = (long long)nsm * BGK_BK_MINBLOCKS;
+  int per = bgk::kBkPerThread;
+  long long best = LLONG_MAX;
+  const int pmin = n <= 2 * slots * bgk::kBkChunk ? bgk::kBkPerThread - 3 : bgk::kBkPerThread;
+  for (int p = bgk::kBkPerThread; p >= pmin && p >= 1; --p) {
+    const long long ctas = (n + (long long)bgk::kBkThreads * p - 1) / ((long long)bgk::kBkThreads * p);
+    const long long cost = (ctas + slots - 1) / slots * p;
+    if (cost < best) {
+      best = cost;
+      per = p;
+    }
+  }
+  const long long grid = (n + (long long)bgk::kBkThreads * per - 1) / ((long long)bgk::kBkThreads * per);
+  const size_t table_bytes = sizeof(double2) * (A.table_ok ? (size_t)cfg->bins + 1 : 0);
+  switch (per - bgk::kBkPerThread) {
+#define BGK_BK_LAUNCH(D)                                                                          \
+  case D: {                                                                                       \
+    constexpr int P = bgk::kBkPerThread + (D);                                                   \
+    const void *fn = (const void *)bgk::besselk_kernel<P>;                                        \
+    /* opt in once per device for the largest table (so every bins <= kMaxTable fits) */          \
+    if (int rc = bgk_ensure_smem_optin(fn, "besselk_kernel",                                      \
+                                       (int)(sizeof(double2) * (kMaxTable + 1) + bgk::bk_chunk_bytes(P)))) \
+      return rc;                                                                                  \
+    bgk::besselk_kernel<P><<<(unsigned)grid, bgk::kBkThreads, table_bytes + bgk::bk_chunk_bytes(P), stream>>>(A); \
+    break;                                                                                        \
+  }
+    BGK_BK_LAUNCH(0)
+    BGK_BK_LAUNCH(-1)
+    BGK_BK_LAUNCH(-2)
+    BGK_BK_LAUNCH(-3)
+#undef BGK_BK_LAUNCH
+    default:
+      bgk_set_error("besselk launch: no kernel for %d elements per thread", per);
+      return BGK_ERR_UNSUPPORTED;
+  }
   bgk_note_launch();
   return bgk_check_launch("besselk_kernel");
 }
