@@ -869,6 +869,9 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
       per = p;
     }
   }
+#ifdef BGK_BK_FORCE_PER  // A/B builds only (BK 1M on B200: the choice above, 7 -> 38 us; 6 / 4 / 3 / 2 -> 40 / 42 / 45 / 48 us)
+  per = BGK_BK_FORCE_PER;
+#endif
   const long long grid = (n + (long long)bgk::kBkThreads * per - 1) / ((long long)bgk::kBkThreads * per);
   const size_t table_bytes = sizeof(double2) * (A.table_ok ? (size_t)cfg->bins + 1 : 0);
   switch (per - bgk::kBkPerThread) {
@@ -887,6 +890,11 @@ int bgk_launch_besselk(const double *x, const double *nu, int64_t n, const bgk_c
     BGK_BK_LAUNCH(-1)
     BGK_BK_LAUNCH(-2)
     BGK_BK_LAUNCH(-3)
+#ifdef BGK_BK_FORCE_PER
+    BGK_BK_LAUNCH(-4)
+    BGK_BK_LAUNCH(-5)
+    BGK_BK_LAUNCH(-6)
+#endif
 #undef BGK_BK_LAUNCH
     default:
       bgk_set_error("besselk launch: no kernel for %d elements per thread", per);

@@ -106,11 +106,13 @@ Window window_at(const bgk_matern_plan &P, double u) {
 // no safe LUT can be built.
 bool build_lut_at(bgk_matern_plan &P, int shift);
 void build_lut(bgk_matern_plan &P) {
-  // 32 buckets per octave (key shift 15) when the table fits, else 16: the tighter
-  // windows now pay for the larger histogram (A/B on B200, v18 kernels: M100
-  // 88.88 vs 89.45 ms, M50 -0.4%); BGK_LUT_KEY_SHIFT=16 forces 16 per octave.
+  // 16 buckets per octave (key shift 16); BGK_LUT_KEY_SHIFT=15 asks for 32 when the
+  // table fits.  A/B on B200: with the round-1 kernels and the e^-40 cut 32 per octave
+  // won (M100 88.88 vs 89.45 ms); with the e^-33 cut the windows change less per
+  // bucket and 16 per octave wins (M100 71.55 vs 71.91, M50 77.82 vs 78.23, M200
+  // 279.5-280.1 vs 281.0-281.6 ms).
   const char *env = std::getenv("BGK_LUT_KEY_SHIFT");
-  const int first = (env && std::atoi(env) == 16) ? 16 : 15;
+  const int first = (env && std::atoi(env) == 15) ? 15 : 16;
   for (int shift = first; shift <= 16; ++shift)
     if (build_lut_at(P, shift)) return;
 }
