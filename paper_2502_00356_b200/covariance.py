@@ -551,7 +551,7 @@ _MIRROR_MIN_N = 4096
 _MIRROR_POOL = None
 _MIRROR_DIRECT = None  # override of _mirror_direct_blocks (tests / tuning)
 _MIRROR_THREADS = None  # host threads of the mirror (default: 3/4)
-_MIRROR_REVERSE = True  # row blocks bottom-up (A/B: 0.800-0.818 vs 0.813-0.832 s, tools/e2e_reverse_check.py)
+_MIRROR_REVERSE = True  # row blocks bottom-up (A/B: 0.800-0.818 vs 0.813-0.832 s, profiles/r02_microbench.md)
 
 
 def _is_pinned(a: np.ndarray) -> bool:
