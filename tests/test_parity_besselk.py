@@ -214,3 +214,20 @@ def test_host_pipeline_matches_device_path(bg):
     with pytest.raises(bg.DomainError) as single:
         bg.EvalPoint(float(x[n // 3]), float("nan"))
     assert str(first.value) == str(single.value)
+
+
+def test_wide_domain_vs_oracle(bg, oracle):
+    """Beyond the BK configuration: x log-uniform over [0.1, 1e4] and nu over [0, 60]
+    (the fast path's window table covers x up to 2^10; larger x take the full grid).
+    The folded node exponent's running bracket x c_a + nu (t_k - t_a) rounds at
+    ulp(x c_a) per node, so its error grows with x; it stays far inside the tolerance."""
+    rng = np.random.default_rng(7)
+    n = 200_000
+    x = 10.0 ** rng.uniform(-1.0, 4.0, n)
+    nu = 60.0 * rng.random(n)
+    r = _lnk(bg, x, nu)
+    ref = oracle.refined_log_bessel_batch(x, nu, threads=8)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(r.log_value), fin)
+    err = np.abs(r.log_value[fin] - ref[fin]) / np.maximum(1.0, np.abs(ref[fin]))
+    assert np.max(err) <= TOL, (np.max(err), x[fin][np.argmax(err)], nu[fin][np.argmax(err)])
